@@ -1,0 +1,106 @@
+/*
+ * rsh.h -- C ABI of librsh.so, the B200 (sm_100a) RSH-SpMM hot path.
+ *
+ * The reference (rstile 0.1.0, /root/reference/pkg/src/rstile) has no native layer: its
+ * boundary is the Python API (__init__.py:79-139).  Each entry point below replaces one
+ * reference function (cited), with the reference's algorithm rewritten as device kernels.
+ *
+ * Conventions
+ *   - every pointer argument is DEVICE memory unless stated; every call is stream-ordered on
+ *     the caller's cudaStream_t and returns before the work completes;
+ *   - the caller owns and allocates every buffer, including workspaces (sized by the matching
+ *     *_workspace / *_bytes query); the library never allocates or frees caller memory;
+ *   - return value: 0 ok, 1 invalid argument (-> ValueError), 2 format (-> FormatError),
+ *     3 CUDA/launch error (-> RuntimeError); rsh_last_error() gives a thread-local message;
+ *   - no global mutable state besides cached per-kernel launch sizes: calls are reentrant,
+ *     one process per GPU for multi-GPU use.
+ *   - dtypes follow the reference format (tile.py:43-82): row_window_id int32,
+ *     row_window_offset int64, bitmaps uint64, col_id int32, values float32; residual row_id
+ *     int32, row_nnz_offset int64, col_id int32, values float32.  CSR: row_ptr int64,
+ *     col_idx int32, values float32 (core.py:26-47).
+ */
+#ifndef RSH_H_
+#define RSH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- plumbing --------------------------------------------------------------------------- */
+const char* rsh_last_error(void);
+int rsh_abi_version(void);
+/* host pointers: compute capability and SM count of the current device */
+int rsh_device_info(int32_t* major, int32_t* minor, int32_t* sms);
+
+/* ---- adaptive row partition: partition.py:119-141 partition_rows (+ column_increment
+ *      partition.py:101-116).  win_start / resid_rows need capacity n_rows (int32);
+ *      counts[0] = #windows, counts[1] = #residual rows (device int64[2]).  Window i covers
+ *      rows [win_start[i], win_start[i] + min(window_size, n_rows - win_start[i])). -------- */
+size_t rsh_partition_workspace(int64_t n_rows);
+int rsh_partition(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, int32_t window_size,
+                  int64_t tau_nnz, int64_t tau_inc, int32_t* win_start, int32_t* resid_rows, int64_t* counts,
+                  void* ws, size_t ws_bytes, cudaStream_t stream);
+
+/* ---- window columns + split_long_work: partition.py:144-180.  win_count may be NULL
+ *      (counts = min(window_size, n_rows - start)).  Outputs: row_win[n_rows] (window of each
+ *      row or -1), prefix[nnz+1] (exclusive scan of first-occurrence flags), nblocks[n_win]
+ *      = ceil(|window_columns|/8), longest[n_win] = longest row, chunk[n_win] = segment
+ *      length (0: unsplit), entry_base/block_base[n_win+1] exclusive scans.
+ *      max_blocks_per_item <= 0 means None. ----------------------------------------------- */
+size_t rsh_plan_workspace(int64_t n_rows, int64_t nnz, int64_t n_win);
+int rsh_plan_windows(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, int64_t nnz,
+                     int32_t window_size, const int32_t* win_start, const int32_t* win_count, int64_t n_win,
+                     int64_t max_blocks_per_item, int32_t split_on_row_nnz, double split_factor, int32_t* row_win,
+                     int32_t* prefix, int64_t* nblocks, int64_t* longest, int64_t* chunk, int64_t* entry_base,
+                     int64_t* block_base, void* ws, size_t ws_bytes, cudaStream_t stream);
+
+/* ---- RS-Tile build: tile.py:102-144 build_rstile (TC part).  With chunk == NULL the
+ *      entry arrays are not written (the caller supplies explicit segments). -------------- */
+size_t rsh_fill_workspace(int64_t nnz, int64_t n_blocks);
+int rsh_build_fill(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
+                   int64_t nnz, int32_t window_size, const int32_t* win_start, const int32_t* win_count,
+                   int64_t n_win, const int32_t* row_win, const int32_t* prefix, const int64_t* block_base,
+                   int64_t n_blocks, const int64_t* chunk, const int64_t* entry_base, int32_t* row_window_id,
+                   int64_t* row_window_offset, uint64_t* bitmaps, int32_t* col_id, float* tc_values, void* ws,
+                   size_t ws_bytes, cudaStream_t stream);
+
+/* ---- residual part: tile.py:146-165 ------------------------------------------------------ */
+size_t rsh_residual_workspace(int64_t n_res);
+int rsh_residual_offsets(const int64_t* row_ptr, const int32_t* resid_rows, int64_t n_res, int64_t* offsets,
+                         void* ws, size_t ws_bytes, cudaStream_t stream);
+int rsh_residual_gather(const int64_t* row_ptr, const int32_t* col_idx, const float* values,
+                        const int32_t* resid_rows, int64_t n_res, const int64_t* offsets, int32_t* res_col_id,
+                        float* res_values, cudaStream_t stream);
+
+/* ---- persistent-kernel schedule: execute.py:136-168 (_window_groups, value starts) as device
+ *      data.  header_out (device int64[8], may be NULL) = [groups, window units, units,
+ *      partial slots, uncovered rows, 0, 0, 0]. ------------------------------------------- */
+size_t rsh_schedule_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res);
+int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_id,
+                 const int64_t* row_window_offset, int64_t n_entries, const uint64_t* bitmaps, int64_t n_blocks,
+                 const int32_t* res_row_id, int64_t n_res, void* sched, size_t sched_bytes, int64_t* header_out,
+                 cudaStream_t stream);
+size_t rsh_partials_bytes(int64_t partial_slots, int64_t n_features, int32_t accum);
+
+/* ---- hybrid SpMM: execute.py:155-218 hybrid_spmm.  C[n_rows x N] (row stride ldc) is
+ *      fully written: window rows assigned, residual rows assigned, all other rows zero.
+ *      B[n_cols x N] row stride ldb; b_dtype 0 f32, 1 bf16, 2 f16; accum 0 f32, 1 f64.
+ *      rsh_spmm_cc: one persistent CUDA-core launch (exact FP32 products). -------------- */
+int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const uint64_t* bitmaps,
+                const int32_t* col_id, const float* tc_values, int64_t n_blocks, const int32_t* res_row_id,
+                const int64_t* res_offset, const int32_t* res_col_id, const float* res_values, int64_t n_res,
+                const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum,
+                void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
+
+/* ---- verification: core.py:398-408 max_relative_error, result in out[0] (device double) - */
+int rsh_max_relative_error(const float* c, const float* ref, int64_t rows, int64_t n_features, int64_t ldc,
+                           double* out, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSH_H_ */

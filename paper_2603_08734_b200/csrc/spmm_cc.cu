@@ -1,0 +1,563 @@
+// Hybrid RS-Tile SpMM: persistent work-unit scheduler + CUDA-core window/residual/zero paths
+// (north-star subsystems (3) and (4); the tensor-core window path lives in spmm_tc.cu).
+//
+// Reference executor: execute.py:155-226 (hybrid_spmm).  Semantics kept:
+//   * C is written exactly once per row: window rows [rid, rid + min(window_size, n - rid))
+//     are ASSIGNED (execute.py:181-182), residual rows are ASSIGNED (execute.py:191-193), every
+//     other row is zero (execute.py:163) -- zero rows are their own work units, so C is never
+//     memset and then overwritten.
+//   * consecutive entries sharing a row_window_id form one logical window whose block
+//     sequence is independent of how it was split (execute.py:136-152).  Here a logical window
+//     is cut at FIXED block offsets (kChunk blocks) from its first block; chunk partials are
+//     summed in chunk order by whichever warp finishes last (atomic ticket), so the result is
+//     bit-identical for every max_blocks_per_item and every scheduling order.
+//   * accumulate_precision f32 / f64 (execute.py:33-49): AccT = float / double.
+#include "common.cuh"
+#include <cub/cub.cuh>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+namespace rsh {
+
+constexpr int kChunk = 32;      // blocks per window work unit
+constexpr int kResRows = 8;     // residual rows per unit
+constexpr int kZeroRows = 32;   // uncovered rows per unit
+
+enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
+
+// header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
+// counters: uint32 [0]=next unit [1]=warps done
+struct Sched {
+  int64_t* header;
+  uint32_t* counters;
+  int32_t *head, *grp_rid, *grp_b0, *grp_b1, *grp_nch, *grp_multi, *grp_slot, *unit_base, *slot_base;
+  uint32_t* ticket;
+  int32_t* vstart;
+  uint8_t* flags;
+  int32_t* pc;
+  uint8_t* uncov_flag;
+  int32_t* uncovered;
+  int4* units;
+  void* cub;
+  size_t cub_bytes;
+  int64_t max_units;
+};
+
+size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res, Sched* s) {
+  Carve cv(base);
+  int64_t E = n_entries;
+  s->header = cv.take<int64_t>(8);
+  s->counters = cv.take<uint32_t>(4);
+  s->head = cv.take<int32_t>(E + 1);
+  s->grp_rid = cv.take<int32_t>(E + 1);
+  s->grp_b0 = cv.take<int32_t>(E + 1);
+  s->grp_b1 = cv.take<int32_t>(E + 1);
+  s->grp_nch = cv.take<int32_t>(E + 1);
+  s->grp_multi = cv.take<int32_t>(E + 1);
+  s->grp_slot = cv.take<int32_t>(E + 1);
+  s->unit_base = cv.take<int32_t>(E + 1);
+  s->slot_base = cv.take<int32_t>(E + 1);
+  s->ticket = cv.take<uint32_t>(E + 1);
+  s->vstart = cv.take<int32_t>(n_blocks + 1);
+  int64_t big = n_rows > E ? n_rows : E;
+  big = big > n_blocks ? big : n_blocks;
+  s->flags = cv.take<uint8_t>(big + 1);
+  s->pc = cv.take<int32_t>(n_blocks + 1);
+  s->uncov_flag = cv.take<uint8_t>(n_rows + 1);
+  s->uncovered = cv.take<int32_t>(n_rows + 1);
+  s->max_units = E + n_blocks / kChunk + 1 + (n_res + kResRows - 1) / kResRows + (n_rows + kZeroRows - 1) / kZeroRows + 4;
+  s->units = cv.take<int4>(s->max_units);
+  size_t a = 0, b = 0;
+  cub::DeviceSelect::Flagged(nullptr, a, cub::CountingInputIterator<int32_t>(0), (uint8_t*)nullptr, (int32_t*)nullptr,
+                             (int64_t*)nullptr, (int)(big + 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int)(big + 1));
+  s->cub_bytes = a > b ? a : b;
+  s->cub = cv.take<char>(s->cub_bytes);
+  return cv.used + 256;
+}
+
+// ------------------------------------------------------------------------------------------
+// schedule construction
+// ------------------------------------------------------------------------------------------
+
+__global__ void k_group_heads(const int32_t* __restrict__ rwid, int64_t E, uint8_t* flag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    flag[e] = (e == 0 || rwid[e] != rwid[e - 1]);
+}
+
+__global__ void k_groups(const int32_t* __restrict__ rwid, const int64_t* __restrict__ rwoff, int64_t E, Sched s) {
+  int64_t G = s.header[0];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= E; g += (int64_t)gridDim.x * blockDim.x) {
+    int32_t nch = 0, multi = 0;
+    if (g < G) {
+      int64_t e0 = s.head[g], e1 = g + 1 < G ? s.head[g + 1] : E;
+      int64_t b0 = rwoff[e0], b1 = rwoff[e1];
+      s.grp_rid[g] = rwid[e0];
+      s.grp_b0[g] = (int32_t)b0;
+      s.grp_b1[g] = (int32_t)b1;
+      int64_t c = (b1 - b0 + kChunk - 1) / kChunk;
+      nch = (int32_t)(c > 1 ? c : 1);
+      multi = nch > 1 ? nch : 0;
+      s.grp_nch[g] = nch;
+      s.ticket[g] = 0;
+    }
+    s.grp_multi[g] = multi;
+    s.unit_base[g] = nch;  // scanned in place afterwards (copied through cub)
+  }
+}
+
+__global__ void k_window_units(int64_t E, Sched s) {
+  int64_t G = s.header[0];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    int32_t nch = s.grp_nch[g], b0 = s.grp_b0[g], b1 = s.grp_b1[g];
+    int32_t base = s.unit_base[g];
+    s.grp_slot[g] = nch > 1 ? s.slot_base[g] : -1;
+    for (int32_t k = 0; k < nch; ++k) {
+      int32_t lo = b0 + k * kChunk, hi = lo + kChunk < b1 ? lo + kChunk : b1;
+      s.units[base + k] = make_int4(kUnitWindow | (k << 2), (int32_t)g, lo, hi);
+    }
+  }
+}
+
+__global__ void k_uncover(Sched s, int64_t n_rows, int window_size, const int32_t* __restrict__ res_row, int64_t n_res) {
+  int64_t G = s.header[0];
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g = tid; g < G; g += stride) {
+    int64_t rid = s.grp_rid[g];
+    int64_t avail = window_size < n_rows - rid ? window_size : n_rows - rid;
+    for (int64_t i = 0; i < avail; ++i) s.uncov_flag[rid + i] = 0;
+  }
+  for (int64_t i = tid; i < n_res; i += stride) s.uncov_flag[res_row[i]] = 0;
+}
+
+__global__ void k_popc32(const unsigned long long* __restrict__ bm, int64_t nb, int32_t* pc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nb; i += (int64_t)gridDim.x * blockDim.x)
+    pc[i] = i < nb ? __popcll(bm[i]) : 0;
+}
+
+__global__ void k_finish_header(Sched s, int64_t E, int64_t n_res) {
+  int64_t uw = s.unit_base[E];
+  int64_t ru = (n_res + kResRows - 1) / kResRows;
+  int64_t z = s.header[4];
+  int64_t zu = (z + kZeroRows - 1) / kZeroRows;
+  s.header[1] = uw;
+  s.header[2] = uw + ru + zu;
+  s.header[3] = s.slot_base[E];
+  s.counters[0] = 0;
+  s.counters[1] = 0;
+}
+
+__global__ void k_tail_units(Sched s, int64_t n_res) {
+  int64_t uw = s.header[1], z = s.header[4];
+  int64_t ru = (n_res + kResRows - 1) / kResRows, zu = (z + kZeroRows - 1) / kZeroRows;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ru + zu; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < ru) {
+      int64_t lo = i * kResRows, hi = lo + kResRows < n_res ? lo + kResRows : n_res;
+      s.units[uw + i] = make_int4(kUnitResidual, (int32_t)lo, (int32_t)hi, 0);
+    } else {
+      int64_t j = i - ru;
+      int64_t lo = j * kZeroRows, hi = lo + kZeroRows < z ? lo + kZeroRows : z;
+      s.units[uw + i] = make_int4(kUnitZero, (int32_t)lo, (int32_t)hi, 0);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// vector load / store helpers (VEC consecutive features per lane)
+// ------------------------------------------------------------------------------------------
+
+template <class BT>
+__device__ __forceinline__ float to_f(BT x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <>
+__device__ __forceinline__ float to_f<__half>(__half x) { return __half2float(x); }
+
+template <int VEC, class BT>
+__device__ __forceinline__ void load_vec(const BT* __restrict__ p, float (&o)[VEC]) {
+  constexpr int bytes = VEC * (int)sizeof(BT);
+  if constexpr (bytes % 16 == 0) {
+#pragma unroll
+    for (int q = 0; q < bytes / 16; ++q) {
+      uint4 u = __ldg(reinterpret_cast<const uint4*>(p) + q);
+      const BT* e = reinterpret_cast<const BT*>(&u);
+#pragma unroll
+      for (int t = 0; t < 16 / (int)sizeof(BT); ++t) o[q * (16 / sizeof(BT)) + t] = to_f<BT>(e[t]);
+    }
+  } else if constexpr (bytes == 8) {
+    uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    const BT* e = reinterpret_cast<const BT*>(&u);
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) o[t] = to_f<BT>(e[t]);
+  } else if constexpr (bytes == 4) {
+    uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(p));
+    const BT* e = reinterpret_cast<const BT*>(&u);
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) o[t] = to_f<BT>(e[t]);
+  } else {
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) o[t] = to_f<BT>(p[t]);
+  }
+}
+
+template <int VEC, class AccT>
+__device__ __forceinline__ void store_c(float* __restrict__ p, const AccT (&a)[VEC]) {
+  if constexpr (VEC % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < VEC / 4; ++q)
+      __stcs(reinterpret_cast<float4*>(p) + q, make_float4((float)a[4 * q], (float)a[4 * q + 1], (float)a[4 * q + 2],
+                                                           (float)a[4 * q + 3]));
+  } else if constexpr (VEC == 2) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2((float)a[0], (float)a[1]));
+  } else {
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) __stcs(p + t, (float)a[t]);
+  }
+}
+
+struct SpmmArgs {
+  const unsigned long long* bitmaps;
+  const int32_t* col_id;
+  const float* tc_values;
+  const int32_t* res_row;
+  const int64_t* res_off;
+  const int32_t* res_col;
+  const float* res_val;
+  const void* B;
+  int64_t ldb;
+  float* C;
+  int64_t ldc;
+  int64_t n_rows;
+  int32_t N;
+  int32_t window_size;
+  Sched s;
+  void* partials;
+};
+
+// ------------------------------------------------------------------------------------------
+// the persistent CUDA-core kernel: one warp per work unit, units fetched dynamically
+// ------------------------------------------------------------------------------------------
+
+template <int VEC, class BT, class AccT>
+__device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int32_t b1, int f0, bool active,
+                                             AccT (&acc)[8][VEC]) {
+  const int lane = threadIdx.x & 31;
+  const BT* B = reinterpret_cast<const BT*>(a.B);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) acc[i][t] = AccT(0);
+  int32_t vp = a.s.vstart[b0];
+  for (int32_t blk = b0; blk < b1; ++blk) {
+    unsigned long long bm = __ldg(a.bitmaps + blk);
+    int32_t colreg = lane < 8 ? __ldg(a.col_id + (int64_t)blk * 8 + lane) : 0;
+    int nv = __popcll(bm);
+    float v0 = lane < nv ? __ldg(a.tc_values + vp + lane) : 0.f;
+    float v1 = lane + 32 < nv ? __ldg(a.tc_values + vp + 32 + lane) : 0.f;
+    int kk = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t rb = uint32_t(bm >> (8 * i)) & 0xffu;
+      while (rb) {
+        int j = __ffs(rb) - 1;
+        rb &= rb - 1;
+        int32_t c = __shfl_sync(0xffffffffu, colreg, j);
+        float va = __shfl_sync(0xffffffffu, v0, kk & 31);
+        float vb = __shfl_sync(0xffffffffu, v1, kk & 31);
+        AccT v = AccT(kk < 32 ? va : vb);
+        ++kk;
+        if (active) {
+          float bv[VEC];
+          load_vec<VEC, BT>(B + (int64_t)c * a.ldb + f0, bv);
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) acc[i][t] = fma(v, AccT(bv[t]), acc[i][t]);
+        }
+      }
+    }
+    vp += nv;
+  }
+}
+
+template <int VEC, class BT, class AccT>
+__global__ void __launch_bounds__(kThreads) k_spmm_cc(SpmmArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total_units = a.s.header[2];
+  const int n_fc = (a.N + 32 * VEC - 1) / (32 * VEC);
+  const BT* B = reinterpret_cast<const BT*>(a.B);
+  for (;;) {
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(a.s.counters, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if ((int64_t)u >= total_units) break;
+    int4 un = a.s.units[u];
+    int type = un.x & 3;
+    if (type == kUnitWindow) {
+      int32_t g = un.y, k = un.x >> 2;
+      int64_t rid = a.s.grp_rid[g];
+      int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
+      int32_t slot = a.s.grp_slot[g];
+      for (int fc = 0; fc < n_fc; ++fc) {
+        int f0 = fc * 32 * VEC + lane * VEC;
+        bool active = f0 < a.N;
+        AccT acc[8][VEC];
+        window_chunk<VEC, BT, AccT>(a, un.z, un.w, f0, active, acc);
+        if (slot < 0) {
+          if (active) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i < avail) store_c<VEC, AccT>(a.C + (rid + i) * a.ldc + f0, acc[i]);
+          }
+        } else if (active) {
+          AccT* part = reinterpret_cast<AccT*>(a.partials) + ((int64_t)(slot + k) * 8) * a.N;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) __stcg(part + (int64_t)i * a.N + f0 + t, acc[i][t]);
+        }
+      }
+      if (slot >= 0) {
+        __threadfence();
+        __syncwarp();
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(a.s.ticket + g, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        int32_t nch = a.s.grp_nch[g];
+        if ((int32_t)t == nch - 1) {
+          __threadfence();
+          for (int fc = 0; fc < n_fc; ++fc) {
+            int f0 = fc * 32 * VEC + lane * VEC;
+            if (f0 >= a.N) continue;
+            for (int i = 0; i < avail; ++i) {
+              AccT sum[VEC];
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) sum[q] = AccT(0);
+              for (int kk = 0; kk < nch; ++kk) {
+                const AccT* part = reinterpret_cast<const AccT*>(a.partials) + ((int64_t)(slot + kk) * 8 + i) * a.N + f0;
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) sum[q] += __ldcg(part + q);
+              }
+              store_c<VEC, AccT>(a.C + (rid + i) * a.ldc + f0, sum);
+            }
+          }
+          if (lane == 0) a.s.ticket[g] = 0;
+        }
+      }
+    } else if (type == kUnitResidual) {
+      for (int32_t i = un.y; i < un.z; ++i) {
+        int64_t r = a.res_row[i];
+        int64_t s0 = a.res_off[i], s1 = a.res_off[i + 1];
+        for (int fc = 0; fc < n_fc; ++fc) {
+          int f0 = fc * 32 * VEC + lane * VEC;
+          bool active = f0 < a.N;
+          AccT acc[VEC];
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) acc[t] = AccT(0);
+          for (int64_t base = s0; base < s1; base += 32) {
+            int64_t p = base + lane;
+            int32_t cr = p < s1 ? __ldg(a.res_col + p) : 0;
+            float vr = p < s1 ? __ldg(a.res_val + p) : 0.f;
+            int cnt = s1 - base < 32 ? int(s1 - base) : 32;
+            for (int q = 0; q < cnt; ++q) {
+              int32_t c = __shfl_sync(0xffffffffu, cr, q);
+              AccT v = AccT(__shfl_sync(0xffffffffu, vr, q));
+              if (active) {
+                float bv[VEC];
+                load_vec<VEC, BT>(B + (int64_t)c * a.ldb + f0, bv);
+#pragma unroll
+                for (int t = 0; t < VEC; ++t) acc[t] = fma(v, AccT(bv[t]), acc[t]);
+              }
+            }
+          }
+          if (active) store_c<VEC, AccT>(a.C + r * a.ldc + f0, acc);
+        }
+      }
+    } else {
+      for (int32_t j = un.y; j < un.z; ++j) {
+        int64_t r = a.s.uncovered[j];
+        for (int f = lane * VEC; f < a.N; f += 32 * VEC) {
+          AccT z[VEC];
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) z[t] = AccT(0);
+          store_c<VEC, AccT>(a.C + r * a.ldc + f, z);
+        }
+      }
+    }
+  }
+  // last warp out rewinds the counters so the next launch needs no memset
+  __syncwarp();
+  if (lane == 0) {
+    uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
+    if (atomicAdd(a.s.counters + 1, 1u) == total_warps - 1) {
+      a.s.counters[0] = 0;
+      a.s.counters[1] = 0;
+    }
+  }
+}
+
+__global__ void k_max_rel(const float* __restrict__ c, const float* __restrict__ r, int64_t rows, int64_t N,
+                          int64_t ldc, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * N; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = i / N, f = i % N;
+    double x = c[row * ldc + f], y = r[row * ldc + f];
+    double d = fabs(x - y) / fmax(fabs(y), 1.0);
+    m = fmax(m, d);
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+template <int VEC, class BT, class AccT>
+int launch_cc(const SpmmArgs& a, cudaStream_t st) {
+  static int blocks = 0;
+  if (!blocks) {
+    int per_sm = 0;
+    RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm_cc<VEC, BT, AccT>, kThreads, 0));
+    RSH_CUDA(cudaFuncSetAttribute(k_spmm_cc<VEC, BT, AccT>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    blocks = (per_sm > 0 ? per_sm : 1) * sm_count();
+  }
+  k_spmm_cc<VEC, BT, AccT><<<blocks, kThreads, 0, st>>>(a);
+  RSH_LAUNCHED("k_spmm_cc");
+  return kOk;
+}
+
+template <class BT, class AccT>
+int dispatch_vec(const SpmmArgs& a, int vec, cudaStream_t st) {
+  switch (vec) {
+    case 8: return launch_cc<8, BT, AccT>(a, st);
+    case 4: return launch_cc<4, BT, AccT>(a, st);
+    case 2: return launch_cc<2, BT, AccT>(a, st);
+    default: return launch_cc<1, BT, AccT>(a, st);
+  }
+}
+
+}  // namespace rsh
+
+using namespace rsh;
+
+extern "C" {
+
+size_t rsh_schedule_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res) {
+  Sched s;
+  return sched_layout(nullptr, n_rows, n_entries, n_blocks, n_res, &s);
+}
+
+// Work-unit schedule for one RS-Tile format (execute.py:136-168 restated as device data):
+// logical windows, fixed-offset chunks, partial slots, per-block value starts, uncovered rows.
+// header_out (device int64[8]) receives [groups, window units, units, partial slots, uncovered].
+int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_id, const int64_t* row_window_offset,
+                 int64_t n_entries, const uint64_t* bitmaps, int64_t n_blocks, const int32_t* res_row_id, int64_t n_res,
+                 void* sched, size_t sched_bytes, int64_t* header_out, cudaStream_t st) {
+  if (n_rows < 0 || n_entries < 0 || n_blocks < 0 || n_res < 0 || window_size < 1 || window_size > 8)
+    return fail(kInvalid, "rsh_schedule: bad sizes");
+  if (n_blocks >= (1LL << 31) || n_rows >= (1LL << 31)) return fail(kInvalid, "rsh_schedule: index limit");
+  Sched s;
+  size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
+  if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_schedule: buffer %zu < %zu bytes", sched_bytes, need);
+  int64_t E = n_entries;
+  RSH_CUDA(cudaMemsetAsync(s.header, 0, 8 * sizeof(int64_t), st));
+  size_t cb;
+  if (E) {
+    k_group_heads<<<grid_1d(E), kThreads, 0, st>>>(row_window_id, E, s.flags);
+    RSH_LAUNCHED("k_group_heads");
+    cb = s.cub_bytes;
+    RSH_CUDA(cub::DeviceSelect::Flagged(s.cub, cb, cub::CountingInputIterator<int32_t>(0), s.flags, s.head,
+                                        s.header, (int)E, st));
+  }
+  k_groups<<<grid_1d(E + 1), kThreads, 0, st>>>(row_window_id, row_window_offset, E, s);
+  RSH_LAUNCHED("k_groups");
+  // unit_base currently holds nch; scan it (through grp_slot as scratch), multi -> slot_base
+  cb = s.cub_bytes;
+  RSH_CUDA(cudaMemcpyAsync(s.grp_slot, s.unit_base, (E + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.grp_slot, s.unit_base, (int)(E + 1), st));
+  cb = s.cub_bytes;
+  RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.grp_multi, s.slot_base, (int)(E + 1), st));
+  if (E) {
+    k_window_units<<<grid_1d(E), kThreads, 0, st>>>(E, s);
+    RSH_LAUNCHED("k_window_units");
+  }
+  // per-block value starts (execute.py:167-168)
+  k_popc32<<<grid_1d(n_blocks + 1), kThreads, 0, st>>>((const unsigned long long*)bitmaps, n_blocks, s.pc);
+  cb = s.cub_bytes;
+  RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.pc, s.vstart, (int)(n_blocks + 1), st));
+  // uncovered rows
+  if (n_rows) {
+    RSH_CUDA(cudaMemsetAsync(s.uncov_flag, 1, n_rows, st));
+    k_uncover<<<grid_1d(E + n_res + 1), kThreads, 0, st>>>(s, n_rows, window_size, res_row_id, n_res);
+    RSH_LAUNCHED("k_uncover");
+    cb = s.cub_bytes;
+    RSH_CUDA(cub::DeviceSelect::Flagged(s.cub, cb, cub::CountingInputIterator<int32_t>(0), s.uncov_flag, s.uncovered,
+                                        s.header + 4, (int)n_rows, st));
+  }
+  k_finish_header<<<1, 1, 0, st>>>(s, E, n_res);
+  k_tail_units<<<grid_1d(n_res / kResRows + n_rows / kZeroRows + 2), kThreads, 0, st>>>(s, n_res);
+  RSH_LAUNCHED("schedule tail");
+  if (header_out) RSH_CUDA(cudaMemcpyAsync(header_out, s.header, 8 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  return kOk;
+}
+
+// bytes of chunk-partial workspace rsh_spmm needs (partial_slots from the schedule header)
+size_t rsh_partials_bytes(int64_t partial_slots, int64_t N, int32_t accum) {
+  return (size_t)(partial_slots > 0 ? partial_slots : 1) * 8 * (size_t)N * (accum ? sizeof(double) : sizeof(float));
+}
+
+// execute.py:155-218.  b_dtype: 0 f32, 1 bf16, 2 f16.  accum: 0 f32, 1 f64.  math: 0 = CUDA-core
+// (fp32 FMA, exact f32 products), 1 = tensor-core window path (see spmm_tc.cu).
+int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
+                const float* tc_values, int64_t n_blocks, const int32_t* res_row_id, const int64_t* res_offset,
+                const int32_t* res_col_id, const float* res_values, int64_t n_res, const void* B, int64_t ldb,
+                int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
+                void* partials, size_t partial_bytes, cudaStream_t st) {
+  if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 1) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  Sched s;
+  size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
+  if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
+  SpmmArgs a;
+  a.bitmaps = (const unsigned long long*)bitmaps;
+  a.col_id = col_id;
+  a.tc_values = tc_values;
+  a.res_row = res_row_id;
+  a.res_off = res_offset;
+  a.res_col = res_col_id;
+  a.res_val = res_values;
+  a.B = B;
+  a.ldb = ldb;
+  a.C = C;
+  a.ldc = ldc;
+  a.n_rows = n_rows;
+  a.N = (int32_t)N;
+  a.window_size = window_size;
+  a.s = s;
+  a.partials = partials;
+  // widest per-lane vector that tiles N and keeps loads aligned
+  size_t esz = b_dtype == 0 ? 4 : 2;
+  int vec = 8;
+  while (vec > 1 && (N % vec || ldb % vec || ldc % vec || 32 * vec > N ||
+                     ((uintptr_t)B % (vec * esz)) || ((uintptr_t)C % (vec * 4 < 16 ? vec * 4 : 16))))
+    vec >>= 1;
+  if (accum == 1 && vec > 4) vec = 4;
+  if (accum == 0) {
+    if (b_dtype == 0) return dispatch_vec<float, float>(a, vec, st);
+    if (b_dtype == 1) return dispatch_vec<__nv_bfloat16, float>(a, vec, st);
+    return dispatch_vec<__half, float>(a, vec, st);
+  }
+  if (b_dtype == 0) return dispatch_vec<float, double>(a, vec, st);
+  if (b_dtype == 1) return dispatch_vec<__nv_bfloat16, double>(a, vec, st);
+  return dispatch_vec<__half, double>(a, vec, st);
+}
+
+// max |c - r| / max(|r|, 1) over rows x N (core.py:398-408), as a double in out[0]
+int rsh_max_relative_error(const float* c, const float* r, int64_t rows, int64_t N, int64_t ldc, double* out,
+                           cudaStream_t st) {
+  RSH_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+  if (rows * N == 0) return kOk;
+  k_max_rel<<<grid_1d(rows * N, kThreads) > 4096 ? 4096 : grid_1d(rows * N), kThreads, 0, st>>>(
+      c, r, rows, N, ldc, (unsigned long long*)out);
+  RSH_LAUNCHED("k_max_rel");
+  return kOk;
+}
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+"""Device-resident RSH-SpMM pipeline: CSR -> partition -> split -> RS-Tile -> schedule -> SpMM.
+
+Every step runs as sm_100a kernels from librsh.so (C ABI, include/rsh.h) on the current torch
+CUDA stream; torch only allocates device memory (caller-owned buffers and workspaces, as the
+ABI requires) and provides the stream.  The host reads back a handful of sizes between the
+build phases (window / block / entry / residual counts) -- nothing else leaves the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, lib
+
+_U64 = np.uint64
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def require_cuda(device=None) -> torch.device:
+    """The product has no CPU path: fail loudly without a CUDA device or the library."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2603_08734_b200 needs a CUDA device (sm_100a); none is available")
+    lib()
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+# ---------------------------------------------------------------------------------------------
+# containers
+# ---------------------------------------------------------------------------------------------
+
+@dataclass
+class DeviceCsr:
+    """CSR resident in HBM with the reference dtypes (int64 row_ptr, int32 col_idx, f32 values)."""
+
+    n_rows: int
+    n_cols: int
+    row_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    values: torch.Tensor
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @property
+    def device(self) -> torch.device:
+        return self.row_ptr.device
+
+    @classmethod
+    def from_host(cls, a, device=None) -> "DeviceCsr":
+        dev = require_cuda(device)
+        return cls(int(a.n_rows), int(a.n_cols),
+                   torch.from_numpy(np.ascontiguousarray(a.row_ptr, np.int64)).to(dev),
+                   torch.from_numpy(np.ascontiguousarray(a.col_idx, np.int32)).to(dev),
+                   torch.from_numpy(np.ascontiguousarray(a.values, np.float32)).to(dev))
+
+
+TILE_FIELDS = ("row_window_id", "row_window_offset", "bitmaps", "col_id", "values",
+               "res_row_id", "res_offset", "res_col_id", "res_values")
+
+
+@dataclass
+class DeviceTile:
+    """An RS-Tile matrix (tile.py:43-91) resident in HBM.  ``bitmaps`` is stored as int64 bits
+    (torch's uint64 support is partial); ``to_host`` reinterprets them as uint64."""
+
+    n_rows: int
+    n_cols: int
+    window_size: int
+    row_window_id: torch.Tensor      # int32 [E]
+    row_window_offset: torch.Tensor  # int64 [E+1]
+    bitmaps: torch.Tensor            # int64 (u64 bits) [nb]
+    col_id: torch.Tensor             # int32 [8 nb]
+    values: torch.Tensor             # float32 [tc nnz]
+    res_row_id: torch.Tensor         # int32 [R]
+    res_offset: torch.Tensor         # int64 [R+1]
+    res_col_id: torch.Tensor         # int32 [res nnz]
+    res_values: torch.Tensor         # float32 [res nnz]
+    _plan: "SpmmPlan | None" = field(default=None, repr=False)
+
+    @property
+    def n_entries(self) -> int:
+        return int(self.row_window_id.numel())
+
+    @property
+    def n_blocks(self) -> int:
+        return int(self.bitmaps.numel())
+
+    @property
+    def n_res(self) -> int:
+        return int(self.res_row_id.numel())
+
+    @property
+    def device(self) -> torch.device:
+        return self.row_window_offset.device
+
+    def nbytes(self) -> int:
+        return sum(getattr(self, f).numel() * getattr(self, f).element_size() for f in TILE_FIELDS)
+
+    def host_arrays(self) -> dict:
+        out = {f: getattr(self, f).cpu().numpy() for f in TILE_FIELDS}
+        out["bitmaps"] = out["bitmaps"].view(_U64)
+        return out
+
+    @classmethod
+    def from_arrays(cls, n_rows, n_cols, window_size, arrays: dict, device=None) -> "DeviceTile":
+        dev = require_cuda(device)
+        dt = {"row_window_id": np.int32, "row_window_offset": np.int64, "bitmaps": np.uint64,
+              "col_id": np.int32, "values": np.float32, "res_row_id": np.int32,
+              "res_offset": np.int64, "res_col_id": np.int32, "res_values": np.float32}
+        ts = {}
+        for f in TILE_FIELDS:
+            a = np.ascontiguousarray(arrays[f], dtype=dt[f])
+            if f == "bitmaps":
+                a = a.view(np.int64)
+            ts[f] = torch.from_numpy(a).to(dev)
+        return cls(int(n_rows), int(n_cols), int(window_size), **ts)
+
+
+# ---------------------------------------------------------------------------------------------
+# build pipeline
+# ---------------------------------------------------------------------------------------------
+
+def partition_device(a: DeviceCsr, window_size: int, tau_nnz: int, tau_inc: int, stream=None):
+    """partition.py:119-141 on device -> (win_start int32, resid_rows int32)."""
+    dev = a.device
+    n = a.n_rows
+    win = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    res = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    nbytes = lib().rsh_partition_workspace(n)
+    ws = _ws(nbytes, dev)
+    call("rsh_partition", _ptr(a.row_ptr), _ptr(a.col_idx), n, window_size, tau_nnz, tau_inc,
+         _ptr(win), _ptr(res), _ptr(counts), _ptr(ws), nbytes, _stream(stream))
+    nw, nr = (int(x) for x in counts.cpu())
+    return win[:nw], res[:nr]
+
+
+@dataclass
+class WindowPlan:
+    """Per-window planning state shared by split_long_work and the build (partition.py:144-180)."""
+
+    win_start: torch.Tensor   # int32 [nw]
+    win_count: torch.Tensor | None  # int32 [nw] explicit row counts, None = min(W, n - start)
+    row_win: torch.Tensor     # int32 [n_rows]
+    prefix: torch.Tensor      # int32 [nnz+1] exclusive scan of first-occurrence flags
+    nblocks: torch.Tensor     # int64 [nw]
+    longest: torch.Tensor     # int64 [nw]
+    chunk: torch.Tensor       # int64 [nw], 0 = unsplit
+    entry_base: torch.Tensor  # int64 [nw+1]
+    block_base: torch.Tensor  # int64 [nw+1]
+    n_entries: int
+    n_blocks: int
+
+
+def plan_windows(a: DeviceCsr, win_start: torch.Tensor, window_size: int, max_blocks_per_item,
+                 split_on_row_nnz: bool = False, split_factor: float = 4.0, stream=None,
+                 win_count: torch.Tensor | None = None) -> WindowPlan:
+    dev = a.device
+    nw = int(win_start.numel())
+    bound = 0 if max_blocks_per_item is None else int(max_blocks_per_item)
+    t64 = lambda k: torch.empty(max(k, 1), dtype=torch.int64, device=dev)  # noqa: E731
+    row_win = torch.empty(max(a.n_rows, 1), dtype=torch.int32, device=dev)
+    prefix = torch.empty(a.nnz + 1, dtype=torch.int32, device=dev)
+    nblocks, longest, chunk = t64(nw), t64(nw), t64(nw)
+    entry_base, block_base = t64(nw + 1), t64(nw + 1)
+    nbytes = lib().rsh_plan_workspace(a.n_rows, a.nnz, nw)
+    ws = _ws(nbytes, dev)
+    call("rsh_plan_windows", _ptr(a.row_ptr), _ptr(a.col_idx), a.n_rows, a.nnz, window_size,
+         _ptr(win_start), _ptr(win_count), nw, bound, int(bool(split_on_row_nnz)), float(split_factor),
+         _ptr(row_win), _ptr(prefix), _ptr(nblocks), _ptr(longest), _ptr(chunk), _ptr(entry_base),
+         _ptr(block_base), _ptr(ws), nbytes, _stream(stream))
+    tot = torch.stack([entry_base[nw], block_base[nw]]).cpu()
+    return WindowPlan(win_start, win_count, row_win, prefix, nblocks[:nw], longest[:nw], chunk[:nw],
+                      entry_base[:nw + 1], block_base[:nw + 1], int(tot[0]), int(tot[1]))
+
+
+def fill_tile(a: DeviceCsr, plan: WindowPlan, resid: torch.Tensor, window_size: int,
+              entries: tuple[np.ndarray, np.ndarray] | None = None, stream=None) -> DeviceTile:
+    """tile.py:102-173 on device.  ``entries`` = explicit (row_window_id, row_window_offset)
+    host arrays for a caller-supplied split map; None = derive them from plan.chunk."""
+    dev = a.device
+    st = _stream(stream)
+    nw = int(plan.win_start.numel())
+    nb = plan.n_blocks
+    if entries is None:
+        ne = plan.n_entries
+        rwid = torch.empty(max(ne, 1), dtype=torch.int32, device=dev)
+        rwoff = torch.empty(ne + 1, dtype=torch.int64, device=dev)
+    else:
+        rwid = torch.from_numpy(np.ascontiguousarray(entries[0], np.int32)).to(dev)
+        rwoff = torch.from_numpy(np.ascontiguousarray(entries[1], np.int64)).to(dev)
+        ne = int(rwid.numel())
+    bitmaps = torch.empty(max(nb, 1), dtype=torch.int64, device=dev)
+    col_id = torch.empty(max(8 * nb, 1), dtype=torch.int32, device=dev)
+    if nw:
+        ws_l = plan.win_start.long()
+        cnt = plan.win_count.long() if plan.win_count is not None else torch.clamp(a.n_rows - ws_l, max=window_size)
+        tc_nnz = int((a.row_ptr[ws_l + cnt] - a.row_ptr[ws_l]).sum())
+    else:
+        tc_nnz = 0
+    values = torch.empty(max(tc_nnz, 1), dtype=torch.float32, device=dev)
+    nbytes = lib().rsh_fill_workspace(a.nnz, nb)
+    ws = _ws(nbytes, dev)
+    call("rsh_build_fill", _ptr(a.row_ptr), _ptr(a.col_idx), _ptr(a.values), a.n_rows, a.nnz,
+         window_size, _ptr(plan.win_start), _ptr(plan.win_count), nw, _ptr(plan.row_win), _ptr(plan.prefix),
+         _ptr(plan.block_base), nb, None if entries is not None else _ptr(plan.chunk),
+         _ptr(plan.entry_base), _ptr(rwid), _ptr(rwoff), _ptr(bitmaps), _ptr(col_id), _ptr(values),
+         _ptr(ws), nbytes, st)
+    # residual part
+    nr = int(resid.numel())
+    r_off = torch.empty(nr + 1, dtype=torch.int64, device=dev)
+    nbytes = lib().rsh_residual_workspace(nr)
+    ws2 = _ws(nbytes, dev)
+    call("rsh_residual_offsets", _ptr(a.row_ptr), _ptr(resid), nr, _ptr(r_off), _ptr(ws2), nbytes, st)
+    r_nnz = int(r_off[nr].item())
+    r_col = torch.empty(max(r_nnz, 1), dtype=torch.int32, device=dev)
+    r_val = torch.empty(max(r_nnz, 1), dtype=torch.float32, device=dev)
+    call("rsh_residual_gather", _ptr(a.row_ptr), _ptr(a.col_idx), _ptr(a.values), _ptr(resid), nr,
+         _ptr(r_off), _ptr(r_col), _ptr(r_val), st)
+    # window_size = max window row count, 8 when there are no windows (tile.py:169-173); only
+    # the last window can be clamped by the matrix edge
+    if nw == 0:
+        wsize = 8
+    elif plan.win_count is not None:
+        wsize = int(plan.win_count.max().item())
+    elif nw >= 2:
+        wsize = window_size
+    else:
+        wsize = min(window_size, a.n_rows - int(plan.win_start[0].item()))
+    return DeviceTile(a.n_rows, a.n_cols, wsize, rwid[:ne], rwoff, bitmaps[:nb], col_id[:8 * nb],
+                      values[:tc_nnz], resid.clone(), r_off, r_col[:r_nnz], r_val[:r_nnz])
+
+
+def build_device(a: DeviceCsr, window_size=8, tau_nnz=None, tau_inc=None, max_blocks_per_item=64,
+                 split_on_row_nnz=False, split_factor=4.0, stream=None) -> DeviceTile:
+    """partition_rows -> split_long_work -> build_rstile, entirely on device."""
+    from .partition import estimate_thresholds
+    if a.n_rows == 0:
+        tn, ti = 0, 0
+    else:
+        est = estimate_thresholds(a.n_rows, a.nnz)
+        tn = est[0] if tau_nnz is None else int(tau_nnz)
+        ti = est[1] if tau_inc is None else int(tau_inc)
+    win, res = partition_device(a, window_size, tn, ti, stream)
+    plan = plan_windows(a, win, window_size, max_blocks_per_item, split_on_row_nnz, split_factor, stream)
+    return fill_tile(a, plan, res, window_size, None, stream)
+
+
+# ---------------------------------------------------------------------------------------------
+# SpMM
+# ---------------------------------------------------------------------------------------------
+
+_BDT = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
+
+
+class SpmmPlan:
+    """Persistent-kernel work schedule of one DeviceTile (built once, reused every call)."""
+
+    def __init__(self, t: DeviceTile, stream=None):
+        dev = t.device
+        self.nbytes = lib().rsh_schedule_bytes(t.n_rows, t.n_entries, t.n_blocks, t.n_res)
+        self.buf = _ws(self.nbytes, dev)
+        hdr = torch.zeros(8, dtype=torch.int64, device=dev)
+        call("rsh_schedule", t.n_rows, t.window_size, _ptr(t.row_window_id), _ptr(t.row_window_offset),
+             t.n_entries, _ptr(t.bitmaps), t.n_blocks, _ptr(t.res_row_id), t.n_res, _ptr(self.buf),
+             self.nbytes, _ptr(hdr), _stream(stream))
+        h = hdr.cpu().tolist()
+        self.groups, self.window_units, self.units, self.partial_slots, self.uncovered = h[:5]
+        self._partials = {}
+
+    def partials(self, N: int, accum: int, dev) -> torch.Tensor:
+        key = (N, accum)
+        if key not in self._partials:
+            nbytes = lib().rsh_partials_bytes(self.partial_slots, N, accum)
+            self._partials[key] = _ws(nbytes, dev)
+        return self._partials[key]
+
+
+def spmm_plan(t: DeviceTile) -> SpmmPlan:
+    if t._plan is None:
+        t._plan = SpmmPlan(t)
+    return t._plan
+
+
+def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None, accumulate: str = "f32",
+                stream=None) -> torch.Tensor:
+    """C = A @ B with A an RS-Tile on device; B [n_cols, N] f32/bf16/f16 row-major on device.
+    Returns (or fills) C [n_rows, N] float32.  accumulate: "f32" | "f64" (execute.py:33-49)."""
+    if b.dim() != 2 or b.shape[0] != t.n_cols:
+        raise ValueError(f"dimension mismatch: matrix has {t.n_cols} columns, B has {tuple(b.shape)}")
+    if b.dtype not in _BDT:
+        raise ValueError(f"unsupported B dtype {b.dtype}")
+    if not b.is_cuda:
+        raise ValueError("B must be a CUDA tensor (use hybrid_spmm for host operands)")
+    if b.stride(1) != 1:
+        b = b.contiguous()
+    N = int(b.shape[1])
+    if out is None:
+        out = torch.empty((t.n_rows, N), dtype=torch.float32, device=b.device)
+    elif out.shape != (t.n_rows, N) or out.dtype != torch.float32 or out.stride(1) != 1:
+        raise ValueError("out must be a float32 [n_rows, N] tensor with unit column stride")
+    if t.n_rows == 0 or N == 0:
+        return out
+    acc = {"f32": 0, "f64": 1}[accumulate]
+    plan = spmm_plan(t)
+    part = plan.partials(N, acc, b.device)
+    call("rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
+         _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),
+         _ptr(t.res_values), t.n_res, _ptr(b), b.stride(0), _BDT[b.dtype], N, _ptr(out), out.stride(0),
+         acc, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
+    return out
+
+
+def max_relative_error_device(c: torch.Tensor, ref: torch.Tensor, stream=None) -> float:
+    out = torch.zeros(1, dtype=torch.float64, device=c.device)
+    call("rsh_max_relative_error", _ptr(c), _ptr(ref), c.shape[0], c.shape[1], c.stride(0), _ptr(out),
+         _stream(stream))
+    return float(out.item())

@@ -12,69 +12,9 @@
 //     summed in chunk order by whichever warp finishes last (atomic ticket), so the result is
 //     bit-identical for every max_blocks_per_item and every scheduling order.
 //   * accumulate_precision f32 / f64 (execute.py:33-49): AccT = float / double.
-#include "common.cuh"
-#include <cub/cub.cuh>
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
+#include "sched.cuh"
 
 namespace rsh {
-
-constexpr int kChunk = 32;      // blocks per window work unit
-constexpr int kResRows = 8;     // residual rows per unit
-constexpr int kZeroRows = 32;   // uncovered rows per unit
-
-enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
-
-// header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
-// counters: uint32 [0]=next unit [1]=warps done
-struct Sched {
-  int64_t* header;
-  uint32_t* counters;
-  int32_t *head, *grp_rid, *grp_b0, *grp_b1, *grp_nch, *grp_multi, *grp_slot, *unit_base, *slot_base;
-  uint32_t* ticket;
-  int32_t* vstart;
-  uint8_t* flags;
-  int32_t* pc;
-  uint8_t* uncov_flag;
-  int32_t* uncovered;
-  int4* units;
-  void* cub;
-  size_t cub_bytes;
-  int64_t max_units;
-};
-
-size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res, Sched* s) {
-  Carve cv(base);
-  int64_t E = n_entries;
-  s->header = cv.take<int64_t>(8);
-  s->counters = cv.take<uint32_t>(4);
-  s->head = cv.take<int32_t>(E + 1);
-  s->grp_rid = cv.take<int32_t>(E + 1);
-  s->grp_b0 = cv.take<int32_t>(E + 1);
-  s->grp_b1 = cv.take<int32_t>(E + 1);
-  s->grp_nch = cv.take<int32_t>(E + 1);
-  s->grp_multi = cv.take<int32_t>(E + 1);
-  s->grp_slot = cv.take<int32_t>(E + 1);
-  s->unit_base = cv.take<int32_t>(E + 1);
-  s->slot_base = cv.take<int32_t>(E + 1);
-  s->ticket = cv.take<uint32_t>(E + 1);
-  s->vstart = cv.take<int32_t>(n_blocks + 1);
-  int64_t big = n_rows > E ? n_rows : E;
-  big = big > n_blocks ? big : n_blocks;
-  s->flags = cv.take<uint8_t>(big + 1);
-  s->pc = cv.take<int32_t>(n_blocks + 1);
-  s->uncov_flag = cv.take<uint8_t>(n_rows + 1);
-  s->uncovered = cv.take<int32_t>(n_rows + 1);
-  s->max_units = E + n_blocks / kChunk + 1 + (n_res + kResRows - 1) / kResRows + (n_rows + kZeroRows - 1) / kZeroRows + 4;
-  s->units = cv.take<int4>(s->max_units);
-  size_t a = 0, b = 0;
-  cub::DeviceSelect::Flagged(nullptr, a, cub::CountingInputIterator<int32_t>(0), (uint8_t*)nullptr, (int32_t*)nullptr,
-                             (int64_t*)nullptr, (int)(big + 1));
-  cub::DeviceScan::ExclusiveSum(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int)(big + 1));
-  s->cub_bytes = a > b ? a : b;
-  s->cub = cv.take<char>(s->cub_bytes);
-  return cv.used + 256;
-}
 
 // ------------------------------------------------------------------------------------------
 // schedule construction
@@ -115,6 +55,7 @@ __global__ void k_window_units(int64_t E, Sched s) {
     for (int32_t k = 0; k < nch; ++k) {
       int32_t lo = b0 + k * kChunk, hi = lo + kChunk < b1 ? lo + kChunk : b1;
       s.units[base + k] = make_int4(kUnitWindow | (k << 2), (int32_t)g, lo, hi);
+      s.unit_cost_raw[base + k] = (hi - lo) + 1;  // blocks gathered + one window of C rows
     }
   }
 }
@@ -161,80 +102,6 @@ __global__ void k_tail_units(Sched s, int64_t n_res) {
     }
   }
 }
-
-// ------------------------------------------------------------------------------------------
-// vector load / store helpers (VEC consecutive features per lane)
-// ------------------------------------------------------------------------------------------
-
-template <class BT>
-__device__ __forceinline__ float to_f(BT x);
-template <>
-__device__ __forceinline__ float to_f<float>(float x) { return x; }
-template <>
-__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
-template <>
-__device__ __forceinline__ float to_f<__half>(__half x) { return __half2float(x); }
-
-template <int VEC, class BT>
-__device__ __forceinline__ void load_vec(const BT* __restrict__ p, float (&o)[VEC]) {
-  constexpr int bytes = VEC * (int)sizeof(BT);
-  if constexpr (bytes % 16 == 0) {
-#pragma unroll
-    for (int q = 0; q < bytes / 16; ++q) {
-      uint4 u = __ldg(reinterpret_cast<const uint4*>(p) + q);
-      const BT* e = reinterpret_cast<const BT*>(&u);
-#pragma unroll
-      for (int t = 0; t < 16 / (int)sizeof(BT); ++t) o[q * (16 / sizeof(BT)) + t] = to_f<BT>(e[t]);
-    }
-  } else if constexpr (bytes == 8) {
-    uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-    const BT* e = reinterpret_cast<const BT*>(&u);
-#pragma unroll
-    for (int t = 0; t < VEC; ++t) o[t] = to_f<BT>(e[t]);
-  } else if constexpr (bytes == 4) {
-    uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(p));
-    const BT* e = reinterpret_cast<const BT*>(&u);
-#pragma unroll
-    for (int t = 0; t < VEC; ++t) o[t] = to_f<BT>(e[t]);
-  } else {
-#pragma unroll
-    for (int t = 0; t < VEC; ++t) o[t] = to_f<BT>(p[t]);
-  }
-}
-
-template <int VEC, class AccT>
-__device__ __forceinline__ void store_c(float* __restrict__ p, const AccT (&a)[VEC]) {
-  if constexpr (VEC % 4 == 0) {
-#pragma unroll
-    for (int q = 0; q < VEC / 4; ++q)
-      __stcs(reinterpret_cast<float4*>(p) + q, make_float4((float)a[4 * q], (float)a[4 * q + 1], (float)a[4 * q + 2],
-                                                           (float)a[4 * q + 3]));
-  } else if constexpr (VEC == 2) {
-    __stcs(reinterpret_cast<float2*>(p), make_float2((float)a[0], (float)a[1]));
-  } else {
-#pragma unroll
-    for (int t = 0; t < VEC; ++t) __stcs(p + t, (float)a[t]);
-  }
-}
-
-struct SpmmArgs {
-  const unsigned long long* bitmaps;
-  const int32_t* col_id;
-  const float* tc_values;
-  const int32_t* res_row;
-  const int64_t* res_off;
-  const int32_t* res_col;
-  const float* res_val;
-  const void* B;
-  int64_t ldb;
-  float* C;
-  int64_t ldc;
-  int64_t n_rows;
-  int32_t N;
-  int32_t window_size;
-  Sched s;
-  void* partials;
-};
 
 // ------------------------------------------------------------------------------------------
 // the persistent CUDA-core kernel: one warp per work unit, units fetched dynamically
@@ -345,44 +212,9 @@ __global__ void __launch_bounds__(kThreads) k_spmm_cc(SpmmArgs a) {
         }
       }
     } else if (type == kUnitResidual) {
-      for (int32_t i = un.y; i < un.z; ++i) {
-        int64_t r = a.res_row[i];
-        int64_t s0 = a.res_off[i], s1 = a.res_off[i + 1];
-        for (int fc = 0; fc < n_fc; ++fc) {
-          int f0 = fc * 32 * VEC + lane * VEC;
-          bool active = f0 < a.N;
-          AccT acc[VEC];
-#pragma unroll
-          for (int t = 0; t < VEC; ++t) acc[t] = AccT(0);
-          for (int64_t base = s0; base < s1; base += 32) {
-            int64_t p = base + lane;
-            int32_t cr = p < s1 ? __ldg(a.res_col + p) : 0;
-            float vr = p < s1 ? __ldg(a.res_val + p) : 0.f;
-            int cnt = s1 - base < 32 ? int(s1 - base) : 32;
-            for (int q = 0; q < cnt; ++q) {
-              int32_t c = __shfl_sync(0xffffffffu, cr, q);
-              AccT v = AccT(__shfl_sync(0xffffffffu, vr, q));
-              if (active) {
-                float bv[VEC];
-                load_vec<VEC, BT>(B + (int64_t)c * a.ldb + f0, bv);
-#pragma unroll
-                for (int t = 0; t < VEC; ++t) acc[t] = fma(v, AccT(bv[t]), acc[t]);
-              }
-            }
-          }
-          if (active) store_c<VEC, AccT>(a.C + r * a.ldc + f0, acc);
-        }
-      }
+      residual_rows<VEC, BT, AccT>(a, un.y, un.z, n_fc);
     } else {
-      for (int32_t j = un.y; j < un.z; ++j) {
-        int64_t r = a.s.uncovered[j];
-        for (int f = lane * VEC; f < a.N; f += 32 * VEC) {
-          AccT z[VEC];
-#pragma unroll
-          for (int t = 0; t < VEC; ++t) z[t] = AccT(0);
-          store_c<VEC, AccT>(a.C + r * a.ldc + f, z);
-        }
-      }
+      zero_rows<VEC>(a, un.y, un.z);
     }
   }
   // last warp out rewinds the counters so the next launch needs no memset
@@ -474,10 +306,13 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.grp_slot, s.unit_base, (int)(E + 1), st));
   cb = s.cub_bytes;
   RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.grp_multi, s.slot_base, (int)(E + 1), st));
+  RSH_CUDA(cudaMemsetAsync(s.unit_cost_raw, 0, (s.max_units + 1) * sizeof(int64_t), st));
   if (E) {
     k_window_units<<<grid_1d(E), kThreads, 0, st>>>(E, s);
     RSH_LAUNCHED("k_window_units");
   }
+  cb = s.cub_bytes;
+  RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.unit_cost_raw, s.unit_cost, (int)(s.max_units + 1), st));
   // per-block value starts (execute.py:167-168)
   k_popc32<<<grid_1d(n_blocks + 1), kThreads, 0, st>>>((const unsigned long long*)bitmaps, n_blocks, s.pc);
   cb = s.cub_bytes;

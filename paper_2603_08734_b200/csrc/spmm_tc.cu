@@ -1,0 +1,461 @@
+// Tensor-core window path (north-star subsystem (2)) inside the persistent hybrid launch (4).
+//
+// Per 8-row window block (the reference's 8x8 bitmap fragment, execute.py:65-89,171-182):
+//   D[f, i] += sum_k B[col_k][f] * Ablk[i][k]      one tcgen05.mma, M = 128 features,
+//                                                  N = 8 window rows, K = 8 (tf32) / 16 (bf16)
+// Operand A  = the 8 gathered B rows, MN-major, 128-byte swizzled canonical layout, staged into
+//              shared memory by cp.async (16-byte, L1-allocating: hot B rows hit in L1) with
+//              zero-fill for padding slots (a col_id slot whose bitmap column is empty);
+// Operand B  = the decoded bitmap block (popc-rank scatter), K-major, rounded to tf32 (cvt.rna);
+// D          = fp32 accumulator in TMEM (8 columns per window, up to 64 windows in flight).
+//
+// Warp roles per CTA (one CTA per SM, persistent, cost-balanced contiguous unit ranges):
+//   warps 0-3   epilogue: tcgen05.ld -> registers -> streaming C stores (or chunk partials +
+//               ordered ticket reduction for windows longer than kChunk blocks)
+//   warp  4     MMA issuer (one lane) + TMEM allocation
+//   warps 5-12  producers: block metadata, gather, decode, mbarrier signalling; afterwards they
+//               take the residual / zero-row units (CUDA-core path) from a global counter.
+#include "sched.cuh"
+
+namespace rsh {
+namespace tc {
+
+constexpr int kEpiWarps = 4;
+constexpr int kMmaWarp = 4;
+constexpr int kProd0 = 5;
+constexpr int kProdWarps = 8;
+constexpr int kThreadsTC = (kProd0 + kProdWarps) * 32;
+constexpr int kTileBytes = 4096;  // A operand bytes per 128-feature tile per block
+constexpr int kBopBytes = 256;    // decoded block (8 rows x 32 B)
+constexpr int kTmemCols = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nRSH_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra RSH_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+}
+
+template <class BT>
+struct Kind;
+template <>
+struct Kind<float> {  // kind::tf32
+  static constexpr uint32_t fmt = 2;
+  static constexpr int eb = 4;
+  static constexpr uint32_t sbo = 4096;
+};
+template <>
+struct Kind<__nv_bfloat16> {  // kind::f16 with bf16 operands, K = 16 (upper 8 zero)
+  static constexpr uint32_t fmt = 1;
+  static constexpr int eb = 2;
+  static constexpr uint32_t sbo = 2048;
+};
+template <>
+struct Kind<__half> {
+  static constexpr uint32_t fmt = 0;
+  static constexpr int eb = 2;
+  static constexpr uint32_t sbo = 2048;
+};
+
+template <class BT>
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (Kind<BT>::eb == 4)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+template <bool kL1>
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  if constexpr (kL1)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// first unit index u in [0, nu] with unit_cost[u] >= target
+__device__ __forceinline__ int64_t cost_bound(const int64_t* __restrict__ cost, int64_t nu, int64_t target) {
+  int64_t lo = 0, hi = nu;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cost[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <class BT, int MT, int STAGES, int DEPTH, bool kL1>
+__global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
+  constexpr int EB = Kind<BT>::eb;
+  constexpr int NACC = kTmemCols / (8 * MT) < 64 ? kTmemCols / (8 * MT) : 64;
+  constexpr int kVec = 4 * MT * (4 / EB);  // per-lane features for the CUDA-core tail units
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;                                   // STAGES * MT * 4 KB
+  uint8_t* sB = sA + STAGES * MT * kTileBytes;          // STAGES * 256 B
+  uint64_t* full = (uint64_t*)(sB + STAGES * kBopBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + NACC;
+  uint32_t* misc = (uint32_t*)(tempty + NACC);         // [0] tmem base, [1] ticket broadcast
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // zero operand memory once: padding never leaks stale data, bf16 K-half stays zero
+  for (int i = threadIdx.x * 16; i < STAGES * (MT * kTileBytes + kBopBytes); i += kThreadsTC * 16)
+    *(uint4*)(smem + i) = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int s = 0; s < NACC; ++s) {
+      mbar_init(tfull + s, 1);
+      mbar_init(tempty + s, kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(misc)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = misc[0];
+
+  // this CTA's contiguous, cost-balanced range of window units
+  const int64_t nwu = a.s.header[1];
+  const int64_t total = a.s.unit_cost[nwu];
+  const int64_t G = gridDim.x;
+  const int64_t u0 = cost_bound(a.s.unit_cost, nwu, (total * (int64_t)blockIdx.x) / G);
+  const int64_t u1 = blockIdx.x + 1 == G ? nwu : cost_bound(a.s.unit_cost, nwu, (total * ((int64_t)blockIdx.x + 1)) / G);
+
+  if (warp >= kProd0) {
+    // ---------------------------------------------------------------- producers
+    const int p = warp - kProd0;
+    const BT* B = reinterpret_cast<const BT*>(a.B);
+    const char* Bbytes = reinterpret_cast<const char*>(a.B);
+    const int64_t row_bytes = a.ldb * EB;
+    int64_t j = 0;  // block sequence number within this CTA
+    int64_t pend[DEPTH + 1];
+    int npend = 0;
+    for (int64_t u = u0; u < u1; ++u) {
+      int4 un = a.s.units[u];
+      int32_t b0 = un.z, b1 = un.w;
+      int64_t nb = b1 - b0;
+      int64_t first = ((p - j) % kProdWarps + kProdWarps) % kProdWarps;
+      for (int64_t q = first; q < nb; q += kProdWarps) {
+        const int64_t jj = j + q;
+        const int32_t blk = b0 + (int32_t)q;
+        const int s = (int)(jj % STAGES);
+        const uint32_t ph = (uint32_t)((jj / STAGES) & 1);
+        mbar_wait(empty + s, ph ^ 1);
+        unsigned long long bm = __ldg(a.bitmaps + blk);
+        int32_t colreg = lane < 8 ? __ldg(a.col_id + (int64_t)blk * 8 + lane) : 0;
+        int32_t vs = a.s.vstart[blk];
+        int nv = __popcll(bm);
+        float v0 = lane < nv ? __ldg(a.tc_values + vs + lane) : 0.f;
+        float v1 = lane + 32 < nv ? __ldg(a.tc_values + vs + 32 + lane) : 0.f;
+        unsigned long long x = bm | (bm >> 32);
+        x |= x >> 16;
+        x |= x >> 8;
+        const uint32_t cm = (uint32_t)x & 0xffu;
+        // gather: row k of the block = B[col_k], 16 B per lane per instruction
+        const uint32_t stageA = smem_u32(sA + (size_t)s * MT * kTileBytes);
+        constexpr int kChunksPerTileRow = 8 * EB;  // 16-B chunks of 128 features
+        constexpr int kChunksPerRow = MT * kChunksPerTileRow;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          int32_t col = __shfl_sync(0xffffffffu, colreg, k);
+          uint32_t nbytes = ((cm >> k) & 1u) ? 16u : 0u;
+          const char* src_row = Bbytes + (int64_t)col * row_bytes;
+#pragma unroll
+          for (int cc = lane; cc < kChunksPerRow; cc += 32) {
+            int t = cc / kChunksPerTileRow;
+            int byte = (cc % kChunksPerTileRow) * 16;
+            int ma = byte >> 7, ci = (byte & 127) >> 4;
+            uint32_t dst = stageA + t * kTileBytes + ma * 1024 + k * 128 + ((ci ^ k) << 4);
+            cp16<kL1>(dst, src_row + cc * 16, nbytes);
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // decode: bit pos = local_row * 8 + local_col; value rank = popc(bits below)
+        uint8_t* bop = sB + (size_t)s * kBopBytes;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int pos = lane + 32 * h;
+          bool set = (bm >> pos) & 1ull;
+          int rank = pos ? __popcll(bm & ((1ull << pos) - 1ull)) : 0;
+          float va = __shfl_sync(0xffffffffu, v0, rank & 31);
+          float vb = __shfl_sync(0xffffffffu, v1, rank & 31);
+          float v = set ? (rank < 32 ? va : vb) : 0.f;
+          int i = pos >> 3, k = pos & 7;
+          if constexpr (EB == 4) {
+            *(uint32_t*)(bop + (k >> 2) * 128 + i * 16 + (k & 3) * 4) = to_tf32(v);
+          } else if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
+            *(__nv_bfloat16*)(bop + i * 16 + k * 2) = __float2bfloat16_rn(v);
+          } else {
+            *(__half*)(bop + i * 16 + k * 2) = __float2half_rn(v);
+          }
+        }
+        pend[npend++] = jj;
+        if (npend > DEPTH) {
+          asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH) : "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(full + (int)(pend[0] % STAGES));
+#pragma unroll
+          for (int z = 0; z < DEPTH; ++z) pend[z] = pend[z + 1];
+          --npend;
+        }
+      }
+      j += nb;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0)
+      for (int z = 0; z < npend; ++z) mbar_arrive(full + (int)(pend[z] % STAGES));
+
+    // residual and zero-row units (CUDA-core), fetched dynamically across the grid
+    const int64_t nunits = a.s.header[2];
+    const int n_fc = (a.N + 32 * kVec - 1) / (32 * kVec);
+    for (;;) {
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(a.s.counters, 1u);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      int64_t u = nwu + t;
+      if (u >= nunits) break;
+      int4 un = a.s.units[u];
+      if ((un.x & 3) == kUnitResidual) residual_rows<kVec, BT, float>(a, un.y, un.z, n_fc);
+      else zero_rows<kVec>(a, un.y, un.z);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      uint32_t producers = gridDim.x * kProdWarps;
+      if (atomicAdd(a.s.counters + 1, 1u) == producers - 1) {
+        a.s.counters[0] = 0;
+        a.s.counters[1] = 0;
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = (1u << 4) | (Kind<BT>::fmt << 7) | (Kind<BT>::fmt << 10) | (1u << 15) |
+                                 (1u << 17) | (8u << 24);
+      int64_t j = 0, ua = 0;
+      for (int64_t u = u0; u < u1; ++u, ++ua) {
+        int4 un = a.s.units[u];
+        const int slot = (int)(ua % NACC);
+        mbar_wait(tempty + slot, (uint32_t)(((ua / NACC) & 1) ^ 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (un.z == un.w) {
+          mbar_arrive(tfull + slot);
+          continue;
+        }
+        for (int32_t blk = un.z; blk < un.w; ++blk, ++j) {
+          const int s = (int)(j % STAGES);
+          mbar_wait(full + s, (uint32_t)((j / STAGES) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t bdesc = umma_desc(smem_u32(sB + (size_t)s * kBopBytes), 128, 256, 0);
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const uint64_t adesc =
+                umma_desc(smem_u32(sA + ((size_t)s * MT + t) * kTileBytes), 1024, Kind<BT>::sbo, 2);
+            mma<BT>(tmem + (uint32_t)((slot * MT + t) * 8), adesc, bdesc, idesc, blk > un.z ? 1u : 0u);
+          }
+          umma_commit(empty + s);
+        }
+        umma_commit(tfull + slot);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 0-3)
+    const int f_in_tile = warp * 32 + lane;
+    int64_t ua = 0;
+    for (int64_t u = u0; u < u1; ++u, ++ua) {
+      int4 un = a.s.units[u];
+      const int slot = (int)(ua % NACC);
+      mbar_wait(tfull + slot, (uint32_t)((ua / NACC) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int32_t g = un.y, k = un.x >> 2;
+      const int64_t rid = a.s.grp_rid[g];
+      const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
+      const int32_t pslot = a.s.grp_slot[g];
+      const bool has = un.z != un.w;
+      float r[MT][8];
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        if (has) {
+          uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((slot * MT + t) * 8);
+          uint32_t q[8];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]),
+                         "=r"(q[7])
+                       : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 8; ++i) r[t][i] = __uint_as_float(q[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) r[t][i] = 0.f;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + slot);
+      if (pslot < 0) {
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int64_t f = t * 128 + f_in_tile;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i < avail) __stcs(a.C + (rid + i) * a.ldc + f, r[t][i]);
+        }
+      } else {
+        float* part = reinterpret_cast<float*>(a.partials) + ((int64_t)(pslot + k) * 8) * a.N;
+#pragma unroll
+        for (int t = 0; t < MT; ++t)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) __stcg(part + (int64_t)i * a.N + t * 128 + f_in_tile, r[t][i]);
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (threadIdx.x == 0) misc[1] = atomicAdd(a.s.ticket + g, 1u);
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        const int32_t nch = a.s.grp_nch[g];
+        if ((int32_t)misc[1] == nch - 1) {
+          __threadfence();
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const int64_t f = t * 128 + f_in_tile;
+            for (int i = 0; i < avail; ++i) {
+              float sum = 0.f;
+              for (int kk = 0; kk < nch; ++kk)
+                sum += __ldcg(reinterpret_cast<const float*>(a.partials) + ((int64_t)(pslot + kk) * 8 + i) * a.N + f);
+              __stcs(a.C + (rid + i) * a.ldc + f, sum);
+            }
+          }
+          if (threadIdx.x == 0) a.s.ticket[g] = 0;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      }
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+template <int MT, int STAGES>
+constexpr size_t smem_bytes() {
+  constexpr int NACC = kTmemCols / (8 * MT) < 64 ? kTmemCols / (8 * MT) : 64;
+  return 1024 + (size_t)STAGES * (MT * kTileBytes + kBopBytes) + (2 * STAGES + 2 * NACC) * 8 + 16;
+}
+
+template <class BT, int MT, int STAGES, int DEPTH, bool kL1>
+int launch(const SpmmArgs& a, cudaStream_t st) {
+  auto kern = k_spmm_tc<BT, MT, STAGES, DEPTH, kL1>;
+  constexpr size_t bytes = smem_bytes<MT, STAGES>();
+  static bool init = false;
+  if (!init) {
+    RSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    init = true;
+  }
+  kern<<<sm_count(), kThreadsTC, bytes, st>>>(a);
+  RSH_LAUNCHED("k_spmm_tc");
+  return kOk;
+}
+
+}  // namespace tc
+}  // namespace rsh
+
+using namespace rsh;
+
+extern "C" {
+
+// Tensor-core hybrid SpMM (execute.py:155-218 semantics, TF32 / BF16 / FP16 operands, fp32
+// accumulation).  Requirements: N in {128, 256}, f32 accumulation, 16-byte aligned B rows.
+// l1: 1 = gather through L1 (cp.async.ca), 0 = L2 only (cp.async.cg).
+int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const uint64_t* bitmaps,
+                const int32_t* col_id, const float* tc_values, int64_t n_blocks, const int32_t* res_row_id,
+                const int64_t* res_offset, const int32_t* res_col_id, const float* res_values, int64_t n_res,
+                const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t l1,
+                void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t st) {
+  if (!(N == 128 || N == 256)) return fail(kInvalid, "rsh_spmm_tc: N must be 128 or 256 (got %lld)", (long long)N);
+  if (b_dtype < 0 || b_dtype > 2) return fail(kInvalid, "rsh_spmm_tc: bad b_dtype");
+  size_t eb = b_dtype == 0 ? 4 : 2;
+  if (ldb < N || ldc < N || ((uintptr_t)B & 15) || ((ldb * eb) & 15))
+    return fail(kInvalid, "rsh_spmm_tc: B rows must be 16-byte aligned");
+  Sched s;
+  size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
+  if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm_tc: schedule buffer too small");
+  SpmmArgs a;
+  a.bitmaps = (const unsigned long long*)bitmaps;
+  a.col_id = col_id;
+  a.tc_values = tc_values;
+  a.res_row = res_row_id;
+  a.res_off = res_offset;
+  a.res_col = res_col_id;
+  a.res_val = res_values;
+  a.B = B;
+  a.ldb = ldb;
+  a.C = C;
+  a.ldc = ldc;
+  a.n_rows = n_rows;
+  a.N = (int32_t)N;
+  a.window_size = window_size;
+  a.s = s;
+  a.partials = partials;
+  const int mt = (int)(N / 128);
+  if (b_dtype == 0) {
+    if (mt == 1) return l1 ? tc::launch<float, 1, 40, 3, true>(a, st) : tc::launch<float, 1, 40, 3, false>(a, st);
+    return l1 ? tc::launch<float, 2, 20, 1, true>(a, st) : tc::launch<float, 2, 20, 1, false>(a, st);
+  }
+  if (b_dtype == 1) {
+    if (mt == 1) return l1 ? tc::launch<__nv_bfloat16, 1, 40, 3, true>(a, st) : tc::launch<__nv_bfloat16, 1, 40, 3, false>(a, st);
+    return l1 ? tc::launch<__nv_bfloat16, 2, 20, 1, true>(a, st) : tc::launch<__nv_bfloat16, 2, 20, 1, false>(a, st);
+  }
+  if (mt == 1) return l1 ? tc::launch<__half, 1, 40, 3, true>(a, st) : tc::launch<__half, 1, 40, 3, false>(a, st);
+  return l1 ? tc::launch<__half, 2, 20, 1, true>(a, st) : tc::launch<__half, 2, 20, 1, false>(a, st);
+}
+
+}  // extern "C"

@@ -32,6 +32,13 @@ def _ws(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
+def _upload(arr, dtype, dev) -> torch.Tensor:
+    x = np.ascontiguousarray(arr, dtype=dtype)
+    if not x.flags.writeable:  # reference containers are read-only; torch wants writable memory
+        x = x.copy()
+    return torch.from_numpy(x).to(dev)
+
+
 def require_cuda(device=None) -> torch.device:
     """The product has no CPU path: fail loudly without a CUDA device or the library."""
     if not torch.cuda.is_available():
@@ -65,10 +72,8 @@ class DeviceCsr:
     @classmethod
     def from_host(cls, a, device=None) -> "DeviceCsr":
         dev = require_cuda(device)
-        return cls(int(a.n_rows), int(a.n_cols),
-                   torch.from_numpy(np.ascontiguousarray(a.row_ptr, np.int64)).to(dev),
-                   torch.from_numpy(np.ascontiguousarray(a.col_idx, np.int32)).to(dev),
-                   torch.from_numpy(np.ascontiguousarray(a.values, np.float32)).to(dev))
+        return cls(int(a.n_rows), int(a.n_cols), _upload(a.row_ptr, np.int64, dev),
+                   _upload(a.col_idx, np.int32, dev), _upload(a.values, np.float32, dev))
 
 
 TILE_FIELDS = ("row_window_id", "row_window_offset", "bitmaps", "col_id", "values",
@@ -129,7 +134,7 @@ class DeviceTile:
             a = np.ascontiguousarray(arrays[f], dtype=dt[f])
             if f == "bitmaps":
                 a = a.view(np.int64)
-            ts[f] = torch.from_numpy(a).to(dev)
+            ts[f] = _upload(a, a.dtype, dev)
         return cls(int(n_rows), int(n_cols), int(window_size), **ts)
 
 

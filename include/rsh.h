@@ -96,6 +96,16 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum,
                 void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
 
+/* rsh_spmm_tc: the same contract with the window blocks on the tensor cores (tcgen05.mma,
+ * fp32 accumulation in TMEM): b_dtype 0 -> TF32 operands, 1 -> BF16, 2 -> FP16.  N must be 128
+ * or 256, B rows 16-byte aligned; residual / uncovered rows run on CUDA cores in the same launch.
+ * l1: 1 gathers B rows through L1 (cp.async.ca), 0 through L2 only (cp.async.cg). */
+int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const uint64_t* bitmaps,
+                const int32_t* col_id, const float* tc_values, int64_t n_blocks, const int32_t* res_row_id,
+                const int64_t* res_offset, const int32_t* res_col_id, const float* res_values, int64_t n_res,
+                const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t l1,
+                void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
+
 /* ---- verification: core.py:398-408 max_relative_error, result in out[0] (device double) - */
 int rsh_max_relative_error(const float* c, const float* ref, int64_t rows, int64_t n_features, int64_t ldc,
                            double* out, cudaStream_t stream);

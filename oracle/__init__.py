@@ -39,7 +39,7 @@ _lib = None
 _i64p = ctypes.POINTER(ctypes.c_int64)
 
 
-def build() -> str:
+def compile_lib() -> str:
     """Compile the C restatement (gcc, no GPU needed)."""
     subprocess.run(["bash", os.path.join(_HERE, "build_oracle.sh")], check=True)
     return _SO
@@ -49,7 +49,7 @@ def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(_SO):
-            build()
+            compile_lib()
         L = ctypes.CDLL(_SO)
         vp = ctypes.c_void_p
         L.orc_column_increment.restype = ctypes.c_int64

@@ -12,8 +12,8 @@
 // Warp roles per CTA (one CTA per SM, persistent, cost-balanced contiguous unit ranges):
 //   warps 0-3   epilogue: tcgen05.ld -> registers -> streaming C stores (or chunk partials +
 //               ordered ticket reduction for windows longer than kChunk blocks)
-//   warp  4     MMA issuer (one lane) + TMEM allocation
-//   warps 5-12  producers: block metadata, gather, decode, mbarrier signalling; afterwards they
+//   warps 4-7   MMA issuers (one lane each, one per SM sub-partition) + TMEM allocation
+//   warps 8-19  producers: block metadata, gather, decode, mbarrier signalling; afterwards they
 //               take the residual / zero-row units (CUDA-core path) from a global counter.
 #include "sched.cuh"
 
@@ -21,12 +21,14 @@ namespace rsh {
 namespace tc {
 
 constexpr int kEpiWarps = 4;
-constexpr int kMmaWarp = 4;
-constexpr int kProd0 = 5;
-constexpr int kProdWarps = 8;
+constexpr int kMmaWarp0 = 4;
+constexpr int kMmaWarps = 4;
+constexpr int kProd0 = kMmaWarp0 + kMmaWarps;
+constexpr int kProdWarps = 12;
 constexpr int kThreadsTC = (kProd0 + kProdWarps) * 32;
 constexpr int kTileBytes = 4096;  // A operand bytes per 128-feature tile per block
 constexpr int kBopBytes = 256;    // decoded block (8 rows x 32 B)
+constexpr int kRawBytes = 256;    // packed values of one block (<= 64 floats)
 constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -51,26 +53,43 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
 
+// Operand A (gathered rows) smem layouts, MN-major, one 4 KB tile per 128 features:
+//   tf32: SWIZZLE_128B_BASE32B (layout 1) atoms of 4 K-rows x 128 B with 32-B granules XOR'd by
+//         the row; 4 MN atoms (LBO 512 B) x 2 K groups (SBO 2048 B) for K = 8
+//   bf16/f16: SWIZZLE_128B (layout 2) atoms of 8 K-rows x 128 B with 16-B chunks XOR'd by the
+//         row; 2 MN atoms (LBO 1024 B) x 2 K groups (SBO 2048 B) for K = 16, the second all zero
+// (validated by tools/microbench/umma_probe.cu against a CPU reference)
 template <class BT>
 struct Kind;
 template <>
 struct Kind<float> {  // kind::tf32
   static constexpr uint32_t fmt = 2;
   static constexpr int eb = 4;
-  static constexpr uint32_t sbo = 4096;
+  static constexpr uint32_t layout = 1, lbo = 512, sbo = 2048;
 };
 template <>
 struct Kind<__nv_bfloat16> {  // kind::f16 with bf16 operands, K = 16 (upper 8 zero)
   static constexpr uint32_t fmt = 1;
   static constexpr int eb = 2;
-  static constexpr uint32_t sbo = 2048;
+  static constexpr uint32_t layout = 2, lbo = 1024, sbo = 2048;
 };
 template <>
 struct Kind<__half> {
   static constexpr uint32_t fmt = 0;
   static constexpr int eb = 2;
-  static constexpr uint32_t sbo = 2048;
+  static constexpr uint32_t layout = 2, lbo = 1024, sbo = 2048;
 };
+
+// byte offset inside a 4 KB A tile of 16-B chunk ci (0..7) of MN atom ma for gathered row k
+template <int EB>
+__device__ __forceinline__ uint32_t a_offset(int ma, int k, int ci) {
+  if constexpr (EB == 4) {
+    const int kg = k >> 2, kr = k & 3;
+    return kg * 2048 + ma * 512 + kr * 128 + ((((ci >> 1) ^ kr)) << 5) + ((ci & 1) << 4);
+  } else {
+    return ma * 1024 + k * 128 + ((ci ^ k) << 4);
+  }
+}
 
 template <class BT>
 __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -119,12 +138,13 @@ template <class BT, int MT, int STAGES, int DEPTH, bool kL1>
 __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
   constexpr int EB = Kind<BT>::eb;
   constexpr int NACC = kTmemCols / (8 * MT) < 64 ? kTmemCols / (8 * MT) : 64;
-  constexpr int kVec = 4 * MT * (4 / EB);  // per-lane features for the CUDA-core tail units
+  constexpr int kVec = 4 * MT;  // per-lane features (N = 128 MT) for the CUDA-core tail units
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                                   // STAGES * MT * 4 KB
-  uint8_t* sB = sA + STAGES * MT * kTileBytes;          // STAGES * 256 B
-  uint64_t* full = (uint64_t*)(sB + STAGES * kBopBytes);
+  uint8_t* sB = sA + STAGES * MT * kTileBytes;          // STAGES * 256 B decoded blocks
+  uint8_t* sRaw = sB + STAGES * kBopBytes;              // STAGES * 256 B packed values
+  uint64_t* full = (uint64_t*)(sRaw + STAGES * kRawBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + NACC;
@@ -147,7 +167,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kMmaWarp) {
+  if (warp == kMmaWarp0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(misc)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -166,90 +186,126 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
 
   if (warp >= kProd0) {
     // ---------------------------------------------------------------- producers
+    // The CTA's window units cover one contiguous block range [B0, B1) (units are consecutive
+    // chunks of consecutive entries), consumed by the MMA warp in order j = blk - B0.  Producer
+    // p owns blocks B0 + p + P*i.  Metadata (bitmap, value start, 8 col ids) for 32 of its blocks
+    // is fetched in one coalesced batch (lane l <-> block l); per block the warp then only issues
+    // asynchronous copies -- 8 gathered B rows (16 B per lane per row, zero-filled for padding
+    // slots) and the packed values -- and decodes the block DEPTH blocks later, once its copies
+    // have landed, so no global-memory latency sits on the per-block path.
     const int p = warp - kProd0;
-    const BT* B = reinterpret_cast<const BT*>(a.B);
     const char* Bbytes = reinterpret_cast<const char*>(a.B);
     const int64_t row_bytes = a.ldb * EB;
-    int64_t j = 0;  // block sequence number within this CTA
-    int64_t pend[DEPTH + 1];
+    const int64_t B0 = u0 < u1 ? a.s.units[u0].z : 0;
+    const int64_t B1 = u0 < u1 ? a.s.units[u1 - 1].w : 0;
+    int64_t pj[DEPTH + 1];
+    unsigned long long pb[DEPTH + 1];
     int npend = 0;
-    for (int64_t u = u0; u < u1; ++u) {
-      int4 un = a.s.units[u];
-      int32_t b0 = un.z, b1 = un.w;
-      int64_t nb = b1 - b0;
-      int64_t first = ((p - j) % kProdWarps + kProdWarps) % kProdWarps;
-      for (int64_t q = first; q < nb; q += kProdWarps) {
-        const int64_t jj = j + q;
-        const int32_t blk = b0 + (int32_t)q;
+    auto complete = [&](int64_t jo, unsigned long long bmo) {
+      const int so = (int)(jo % STAGES);
+      const float* raw = reinterpret_cast<const float*>(sRaw + (size_t)so * kRawBytes);
+      uint8_t* bop = sB + (size_t)so * kBopBytes;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int pos = lane + 32 * h;
+        const bool set = (bmo >> pos) & 1ull;
+        const int rank = pos ? __popcll(bmo & ((1ull << pos) - 1ull)) : 0;
+        const float v = set ? raw[rank] : 0.f;
+        const int i = pos >> 3, k = pos & 7;
+        if constexpr (EB == 4) {
+          *(uint32_t*)(bop + (k >> 2) * 128 + i * 16 + (k & 3) * 4) = to_tf32(v);
+        } else if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
+          *(__nv_bfloat16*)(bop + i * 16 + k * 2) = __float2bfloat16_rn(v);
+        } else {
+          *(__half*)(bop + i * 16 + k * 2) = __float2half_rn(v);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full + so);
+    };
+    for (int64_t base = B0 + p; base < B1; base += 32 * kProdWarps) {
+      const int64_t myblk = base + (int64_t)kProdWarps * lane;
+      const bool mine = myblk < B1;
+      const unsigned long long mbm = mine ? __ldg(a.bitmaps + myblk) : 0ull;
+      const int32_t mvs = mine ? __ldg(a.s.vstart + myblk) : 0;
+      int4 mc0 = make_int4(0, 0, 0, 0), mc1 = make_int4(0, 0, 0, 0);
+      if (mine) {
+        mc0 = __ldg(reinterpret_cast<const int4*>(a.col_id + myblk * 8));
+        mc1 = __ldg(reinterpret_cast<const int4*>(a.col_id + myblk * 8) + 1);
+      }
+      const int64_t left = (B1 - base + kProdWarps - 1) / kProdWarps;
+      const int nbatch = left < 32 ? (int)left : 32;
+      for (int l = 0; l < nbatch; ++l) {
+        const int64_t blk = base + (int64_t)kProdWarps * l;
+        const int64_t jj = blk - B0;
         const int s = (int)(jj % STAGES);
-        const uint32_t ph = (uint32_t)((jj / STAGES) & 1);
-        mbar_wait(empty + s, ph ^ 1);
-        unsigned long long bm = __ldg(a.bitmaps + blk);
-        int32_t colreg = lane < 8 ? __ldg(a.col_id + (int64_t)blk * 8 + lane) : 0;
-        int32_t vs = a.s.vstart[blk];
-        int nv = __popcll(bm);
-        float v0 = lane < nv ? __ldg(a.tc_values + vs + lane) : 0.f;
-        float v1 = lane + 32 < nv ? __ldg(a.tc_values + vs + 32 + lane) : 0.f;
+        const unsigned long long bm = __shfl_sync(0xffffffffu, mbm, l);
+        const int32_t vs = __shfl_sync(0xffffffffu, mvs, l);
+        int32_t col[8];
+        col[0] = __shfl_sync(0xffffffffu, mc0.x, l);
+        col[1] = __shfl_sync(0xffffffffu, mc0.y, l);
+        col[2] = __shfl_sync(0xffffffffu, mc0.z, l);
+        col[3] = __shfl_sync(0xffffffffu, mc0.w, l);
+        col[4] = __shfl_sync(0xffffffffu, mc1.x, l);
+        col[5] = __shfl_sync(0xffffffffu, mc1.y, l);
+        col[6] = __shfl_sync(0xffffffffu, mc1.z, l);
+        col[7] = __shfl_sync(0xffffffffu, mc1.w, l);
         unsigned long long x = bm | (bm >> 32);
         x |= x >> 16;
         x |= x >> 8;
         const uint32_t cm = (uint32_t)x & 0xffu;
-        // gather: row k of the block = B[col_k], 16 B per lane per instruction
+        mbar_wait(empty + s, (uint32_t)(((jj / STAGES) & 1) ^ 1));
         const uint32_t stageA = smem_u32(sA + (size_t)s * MT * kTileBytes);
         constexpr int kChunksPerTileRow = 8 * EB;  // 16-B chunks of 128 features
         constexpr int kChunksPerRow = MT * kChunksPerTileRow;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          int32_t col = __shfl_sync(0xffffffffu, colreg, k);
-          uint32_t nbytes = ((cm >> k) & 1u) ? 16u : 0u;
-          const char* src_row = Bbytes + (int64_t)col * row_bytes;
+          const uint32_t nbytes = ((cm >> k) & 1u) ? 16u : 0u;
+          const char* src_row = Bbytes + (int64_t)col[k] * row_bytes;
 #pragma unroll
           for (int cc = lane; cc < kChunksPerRow; cc += 32) {
-            int t = cc / kChunksPerTileRow;
-            int byte = (cc % kChunksPerTileRow) * 16;
-            int ma = byte >> 7, ci = (byte & 127) >> 4;
-            uint32_t dst = stageA + t * kTileBytes + ma * 1024 + k * 128 + ((ci ^ k) << 4);
+            const int t = cc / kChunksPerTileRow;
+            const int byte = (cc % kChunksPerTileRow) * 16;
+            const uint32_t dst = stageA + t * kTileBytes + a_offset<EB>(byte >> 7, k, (byte & 127) >> 4);
             cp16<kL1>(dst, src_row + cc * 16, nbytes);
           }
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        // decode: bit pos = local_row * 8 + local_col; value rank = popc(bits below)
-        uint8_t* bop = sB + (size_t)s * kBopBytes;
+        // packed values of the block -> raw slot (bit order)
+        const int nv = __popcll(bm);
+        const uint32_t rawdst = smem_u32(sRaw + (size_t)s * kRawBytes);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          int pos = lane + 32 * h;
-          bool set = (bm >> pos) & 1ull;
-          int rank = pos ? __popcll(bm & ((1ull << pos) - 1ull)) : 0;
-          float va = __shfl_sync(0xffffffffu, v0, rank & 31);
-          float vb = __shfl_sync(0xffffffffu, v1, rank & 31);
-          float v = set ? (rank < 32 ? va : vb) : 0.f;
-          int i = pos >> 3, k = pos & 7;
-          if constexpr (EB == 4) {
-            *(uint32_t*)(bop + (k >> 2) * 128 + i * 16 + (k & 3) * 4) = to_tf32(v);
-          } else if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
-            *(__nv_bfloat16*)(bop + i * 16 + k * 2) = __float2bfloat16_rn(v);
-          } else {
-            *(__half*)(bop + i * 16 + k * 2) = __float2half_rn(v);
-          }
+          const int q = lane + 32 * h;
+          if (q < nv)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rawdst + q * 4), "l"(a.tc_values + vs + q)
+                         : "memory");
         }
-        pend[npend++] = jj;
-        if (npend > DEPTH) {
-          asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH) : "memory");
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(full + (int)(pend[0] % STAGES));
+        asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll
-          for (int z = 0; z < DEPTH; ++z) pend[z] = pend[z + 1];
+        for (int z = 0; z <= DEPTH; ++z)
+          if (z == npend) {
+            pj[z] = jj;
+            pb[z] = bm;
+          }
+        if (++npend > DEPTH) {
+          asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH) : "memory");
+          __syncwarp();
+          complete(pj[0], pb[0]);
+#pragma unroll
+          for (int z = 0; z < DEPTH; ++z) {
+            pj[z] = pj[z + 1];
+            pb[z] = pb[z + 1];
+          }
           --npend;
         }
       }
-      j += nb;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    if (lane == 0)
-      for (int z = 0; z < npend; ++z) mbar_arrive(full + (int)(pend[z] % STAGES));
+#pragma unroll
+    for (int z = 0; z < DEPTH; ++z)
+      if (z < npend) complete(pj[z], pb[z]);
 
     // residual and zero-row units (CUDA-core), fetched dynamically across the grid
     const int64_t nunits = a.s.header[2];
@@ -272,13 +328,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
         a.s.counters[1] = 0;
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ---------------------------------------------------------------- MMA issuer
+  } else if (warp >= kMmaWarp0) {
+    // ---------------------------------------------------------------- MMA issuers
+    // One elected lane per warp; a tiny M=128 x N=8 MMA costs ~200 cycles of issue latency per
+    // thread (tools/microbench/umma_issue.cu), so four warps (one per SM sub-partition) issue
+    // in parallel, warp w taking the units ua = w (mod 4), each into its own accumulator.
     if (lane == 0) {
       constexpr uint32_t idesc = (1u << 4) | (Kind<BT>::fmt << 7) | (Kind<BT>::fmt << 10) | (1u << 15) |
                                  (1u << 17) | (8u << 24);
-      int64_t j = 0, ua = 0;
-      for (int64_t u = u0; u < u1; ++u, ++ua) {
+      const int mw = warp - kMmaWarp0;
+      const int64_t B0 = u0 < u1 ? a.s.units[u0].z : 0;
+      int64_t ua = mw;
+      for (int64_t u = u0 + mw; u < u1; u += kMmaWarps, ua += kMmaWarps) {
         int4 un = a.s.units[u];
         const int slot = (int)(ua % NACC);
         mbar_wait(tempty + slot, (uint32_t)(((ua / NACC) & 1) ^ 1));
@@ -287,6 +348,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
           mbar_arrive(tfull + slot);
           continue;
         }
+        int64_t j = un.z - B0;
         for (int32_t blk = un.z; blk < un.w; ++blk, ++j) {
           const int s = (int)(j % STAGES);
           mbar_wait(full + s, (uint32_t)((j / STAGES) & 1));
@@ -295,7 +357,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
 #pragma unroll
           for (int t = 0; t < MT; ++t) {
             const uint64_t adesc =
-                umma_desc(smem_u32(sA + ((size_t)s * MT + t) * kTileBytes), 1024, Kind<BT>::sbo, 2);
+                umma_desc(smem_u32(sA + ((size_t)s * MT + t) * kTileBytes), Kind<BT>::lbo, Kind<BT>::sbo,
+                          Kind<BT>::layout);
             mma<BT>(tmem + (uint32_t)((slot * MT + t) * 8), adesc, bdesc, idesc, blk > un.z ? 1u : 0u);
           }
           umma_commit(empty + s);
@@ -379,7 +442,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == kMmaWarp0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
@@ -388,7 +451,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
 template <int MT, int STAGES>
 constexpr size_t smem_bytes() {
   constexpr int NACC = kTmemCols / (8 * MT) < 64 ? kTmemCols / (8 * MT) : 64;
-  return 1024 + (size_t)STAGES * (MT * kTileBytes + kBopBytes) + (2 * STAGES + 2 * NACC) * 8 + 16;
+  return 1024 + (size_t)STAGES * (MT * kTileBytes + kBopBytes + kRawBytes) + (2 * STAGES + 2 * NACC) * 8 + 16;
 }
 
 template <class BT, int MT, int STAGES, int DEPTH, bool kL1>

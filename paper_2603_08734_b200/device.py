@@ -304,10 +304,33 @@ def spmm_plan(t: DeviceTile) -> SpmmPlan:
     return t._plan
 
 
+def tc_eligible(t: DeviceTile, b: torch.Tensor, accumulate: str = "f32") -> bool:
+    """The tensor-core kernel handles N in {128, 256} with f32 accumulation and 16-B aligned rows."""
+    n = int(b.shape[1])
+    eb = b.element_size()
+    return (accumulate == "f32" and n in (128, 256) and b.data_ptr() % 16 == 0 and (b.stride(0) * eb) % 16 == 0)
+
+
+def resolve_math(math: str, b: torch.Tensor, t: DeviceTile, accumulate: str) -> str:
+    """"tc" (tcgen05 window path) or "cc" (CUDA-core FP32 FMA).  fp32 B: exact FP32 unless the
+    caller asks for tf32; bf16 / f16 B: products are exact either way, so the tensor cores run
+    whenever the shape allows."""
+    if math == "fp32" or accumulate != "f32":
+        return "cc"
+    if not tc_eligible(t, b, accumulate):
+        if math == "tf32":
+            raise ValueError("math='tf32' needs N in {128, 256}, f32 accumulation and 16-byte aligned B rows")
+        return "cc"
+    if math == "tf32":
+        return "tc"
+    return "tc" if b.dtype in (torch.bfloat16, torch.float16) else "cc"
+
+
 def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None, accumulate: str = "f32",
-                stream=None) -> torch.Tensor:
+                stream=None, math: str = "auto", l1: bool = True) -> torch.Tensor:
     """C = A @ B with A an RS-Tile on device; B [n_cols, N] f32/bf16/f16 row-major on device.
-    Returns (or fills) C [n_rows, N] float32.  accumulate: "f32" | "f64" (execute.py:33-49)."""
+    Returns (or fills) C [n_rows, N] float32.  accumulate: "f32" | "f64" (execute.py:33-49);
+    math: "auto" | "fp32" (CUDA-core FMA) | "tf32" (tensor cores, see resolve_math)."""
     if b.dim() != 2 or b.shape[0] != t.n_cols:
         raise ValueError(f"dimension mismatch: matrix has {t.n_cols} columns, B has {tuple(b.shape)}")
     if b.dtype not in _BDT:
@@ -326,10 +349,11 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
     acc = {"f32": 0, "f64": 1}[accumulate]
     plan = spmm_plan(t)
     part = plan.partials(N, acc, b.device)
-    call("rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
+    path = resolve_math(math, b, t, accumulate)
+    call("rsh_spmm_tc" if path == "tc" else "rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
          _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),
          _ptr(t.res_values), t.n_res, _ptr(b), b.stride(0), _BDT[b.dtype], N, _ptr(out), out.stride(0),
-         acc, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
+         int(l1) if path == "tc" else acc, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
     return out
 
 

@@ -62,7 +62,8 @@ class ExecConfig:
 
 def _device_spmm(t, b, cfg: ExecConfig, out=None):
     from .device import spmm_device
-    return spmm_device(t, b, out=out, accumulate=cfg.accumulate_precision)
+    math = "fp32" if cfg.math == "fp32" else cfg.math
+    return spmm_device(t, b, out=out, accumulate=cfg.accumulate_precision, math=math)
 
 
 def _verify(t, b, c) -> None:

@@ -1,0 +1,120 @@
+"""CPU, world_size 2 over gloo: the row-shard layer (paper_2603_08734_b200/dist.py).
+
+Checks the host logic the multi-GPU path runs: cost-balanced cuts snapped to rows the global
+scan visits, shard formats that concatenate (row ids rebased) to exactly the global RS-Tile,
+B broadcast from rank 0, and the uneven point-to-point C gather reproducing the 1-process C
+bit for bit.  The per-shard format and product are computed with the CPU oracle here; on GPUs
+the same shard plan feeds the device builder and kernels.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2603_08734_b200 import dist as D
+from paper_2603_08734_b200 import synth
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _matrix():
+    return O.Csr.of(synth.generate_power_law(3000, 2500, 40000, 1.5, seed=21))
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = _matrix()
+        windows, resid = O.partition(a)
+        win_start = np.array([s for s, _ in windows], np.int64)
+        cuts = D.shard_cuts(np.diff(a.row_ptr), D.allowed_cuts(win_start, resid, a.n_rows), world)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        rp, ci, va = D.local_csr(a.row_ptr, a.col_idx, a.values, r0, r1)
+        loc = O.Csr(r1 - r0, a.n_cols, rp, ci, va)
+        lw, lr = D.local_plan(win_start, resid, r0, r1)
+        lwin = tuple((int(s), int(min(8, loc.n_rows - s))) for s in lw)
+        t = O.build(loc, lwin, lr, O.split_map(loc, lwin))
+        # B from rank 0
+        b = torch.zeros((a.n_cols, 16), dtype=torch.float32)
+        if rank == 0:
+            b.copy_(torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, (a.n_cols, 16)).astype(np.float32)))
+        dist.broadcast(b, 0)
+        c_local = torch.from_numpy(O.spmm_f64(loc, b.numpy())[0])
+        full = D.gather_rows(c_local, cuts, rank, world)
+        shard = {k: getattr(t, k) for k in O.Tile.ARRAYS}
+        shard["r0"] = r0
+        gathered = [None] * world
+        dist.all_gather_object(gathered, shard)
+        if rank == 0:
+            q.put({"cuts": cuts.tolist(), "c": full.numpy(), "shards": gathered, "b": b.numpy()})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_row_shard_matches_single_process(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a = _matrix()
+    cuts = res["cuts"]
+    assert cuts[0] == 0 and cuts[-1] == a.n_rows and cuts == sorted(cuts)
+    # balanced: each shard carries roughly half of the nnz + rows cost
+    cost = np.cumsum(np.diff(a.row_ptr) + 1)
+    assert abs(cost[cuts[1] - 1] / cost[-1] - 0.5) < 0.05
+    # shard formats concatenate to the global format
+    g = O.build_format(a)
+    rwid, off, bm, col, val, rrow, roff, rcol, rval = [], [0], [], [], [], [], [0], [], []
+    for sh in res["shards"]:
+        r0 = sh["r0"]
+        rwid.append(sh["row_window_id"] + r0)
+        off.extend((sh["row_window_offset"][1:] + off[-1]).tolist())
+        bm.append(sh["bitmaps"])
+        col.append(sh["col_id"])
+        val.append(sh["values"])
+        rrow.append(sh["res_row_id"] + r0)
+        roff.extend((sh["res_offset"][1:] + roff[-1]).tolist())
+        rcol.append(sh["res_col_id"])
+        rval.append(sh["res_values"])
+    assert np.array_equal(np.concatenate(rwid), g.row_window_id)
+    assert np.array_equal(np.array(off), g.row_window_offset)
+    assert np.array_equal(np.concatenate(bm), g.bitmaps)
+    assert np.array_equal(np.concatenate(col), g.col_id)
+    assert np.array_equal(np.concatenate(val), g.values)
+    assert np.array_equal(np.concatenate(rrow), g.res_row_id)
+    assert np.array_equal(np.array(roff), g.res_offset)
+    assert np.array_equal(np.concatenate(rcol), g.res_col_id)
+    assert np.array_equal(np.concatenate(rval), g.res_values)
+    # gathered C == single-process C, bit for bit
+    c1, _ = O.spmm_f64(a, res["b"])
+    assert res["c"].tobytes() == c1.tobytes()
+
+
+def test_shard_cuts_edge_cases():
+    nnz = np.array([5, 0, 0, 3, 9, 1], np.int64)
+    allowed = np.array([0, 3, 4, 6])
+    cuts = D.shard_cuts(nnz, allowed, 4)
+    assert cuts[0] == 0 and cuts[-1] == 6
+    assert all(c in allowed for c in cuts)
+    assert list(cuts) == sorted(cuts)
+    assert list(D.shard_cuts(np.zeros(0, np.int64), np.array([0, 0]), 2)) == [0, 0, 0]

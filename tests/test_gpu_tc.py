@@ -1,0 +1,128 @@
+"""GPU: the tensor-core (tcgen05) window path.
+
+North-star tolerances (BASELINE.json): relative Frobenius error <= 1e-3 for TF32 operands and
+<= 1e-2 for BF16/FP16 operands against the reference's fp64 result.  Both tensor-core kinds
+also keep the structural contracts: every row written once, zero rows exact, split-granularity
+invariance and run-to-run determinism.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2603_08734_b200")
+torch = pytest.importorskip("torch")
+
+TF32_TOL = 1e-3  # BASELINE.json north_star: TF32 rel-Frobenius vs fp64
+HALF_TOL = 1e-2  # BF16 / FP16
+
+
+def _tile(a, **kw):
+    from paper_2603_08734_b200.device import DeviceCsr, build_device
+    return build_device(DeviceCsr.from_host(a), **kw)
+
+
+def _b(n, d, seed, dtype=torch.float32):
+    x = np.random.default_rng(seed).uniform(-1, 1, (n, d)).astype(np.float32)
+    return torch.from_numpy(x).cuda().to(dtype)
+
+
+@pytest.mark.parametrize("d", [128, 256])
+def test_tf32_matches_fp64_oracle(small_corpus, d):
+    from paper_2603_08734_b200.device import spmm_device
+    for a in small_corpus:
+        t = _tile(a)
+        b = _b(a.n_cols, d, a.nnz)
+        c = spmm_device(t, b, math="tf32").cpu().numpy()
+        _, ref64 = O.spmm_f64(O.Csr.of(a), b.cpu().numpy())
+        assert O.rel_frobenius(c, ref64) <= TF32_TOL
+        # rows outside windows and residual rows are written exactly like the CUDA-core path
+        cc = spmm_device(t, b, math="fp32").cpu().numpy()
+        zero = ~np.abs(ref64).any(axis=1)
+        assert not c[zero].any()
+        assert np.abs(c - cc).max() <= 1e-2 * max(1.0, np.abs(cc).max())
+
+
+@pytest.mark.parametrize("dt", ["bfloat16", "float16"])
+@pytest.mark.parametrize("d", [128, 256])
+def test_half_operands_on_tensor_cores(dt, d):
+    from paper_2603_08734_b200 import synth
+    from paper_2603_08734_b200.device import resolve_math, spmm_device
+    a = synth.generate_power_law(700, 500, 9000, 1.5, seed=3)
+    t = _tile(a)
+    b = _b(500, d, 5, getattr(torch, dt))
+    assert resolve_math("auto", b, t, "f32") == "tc"
+    c = spmm_device(t, b).cpu().numpy()
+    _, ref64 = O.spmm_f64(O.Csr.of(a), b.float().cpu().numpy())
+    err = O.rel_frobenius(c, ref64)
+    assert err <= HALF_TOL
+    # A values of this corpus are not bf16-exact, so the tensor cores see them rounded; the
+    # CUDA-core path keeps them in fp32
+    assert err <= 5e-3
+
+
+def test_tf32_rounding_is_not_truncation():
+    """A values are rounded to tf32 with cvt.rna before the MMA; with a bf16-exact A and B the
+    TF32 product is exact."""
+    from paper_2603_08734_b200 import synth
+    from paper_2603_08734_b200.device import spmm_device
+    a = synth.generate_power_law(256, 256, 4000, 1.5, seed=9)
+    vals = synth.bf16_round(np.asarray(a.values))
+    a = P.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, vals)
+    t = _tile(a)
+    b = _b(256, 128, 1, torch.bfloat16).float()
+    c = spmm_device(t, b, math="tf32").cpu().numpy()
+    _, ref64 = O.spmm_f64(O.Csr.of(a), b.cpu().numpy())
+    assert O.rel_frobenius(c, ref64) <= 1e-6
+
+
+@pytest.mark.parametrize("l1", [True, False])
+def test_tc_split_invariance_and_determinism(l1):
+    from paper_2603_08734_b200 import synth
+    from paper_2603_08734_b200.device import spmm_device
+    a = synth.generate_power_law(128, 4096, 40000, 2.0, seed=11)
+    b = _b(4096, 128, 11)
+    outs = set()
+    for k in (1, 4, 64, None):
+        t = _tile(a, max_blocks_per_item=k)
+        for _ in range(2):
+            outs.add(spmm_device(t, b, math="tf32", l1=l1).cpu().numpy().tobytes())
+    assert len(outs) == 1
+
+
+def test_tc_long_windows_and_residual_mix():
+    """Multi-chunk windows (partials + ordered ticket reduction), residual rows and uncovered
+    rows in one launch."""
+    from paper_2603_08734_b200.device import spmm_device
+    rng = np.random.default_rng(2)
+    dense = np.zeros((300, 6000), np.float32)
+    dense[0, :] = rng.uniform(-1, 1, 6000)           # 750 blocks -> 24 chunks
+    dense[17, rng.choice(6000, 3000, replace=False)] = 1.0
+    for r in range(40, 300, 7):  # single-nonzero rows: delta <= 1 < tau_inc -> residual
+        dense[r, rng.integers(6000)] = rng.uniform(-1, 1)
+    a = P.CsrMatrix.from_dense(dense)
+    t = _tile(a)
+    assert t.n_res > 0
+    b = _b(6000, 256, 3)
+    _, ref64 = O.spmm_f64(O.Csr.of(a), b.cpu().numpy())
+    for _ in range(3):
+        c = spmm_device(t, b, math="tf32").cpu().numpy()
+        assert O.rel_frobenius(c, ref64) <= TF32_TOL
+        zero = ~dense.any(axis=1)
+        assert not c[zero].any()
+
+
+def test_exec_config_tf32_through_host_api(small_corpus):
+    a = small_corpus[5]
+    m = P.build_rstile(a, P.split_long_work(a, P.partition_rows(a)))
+    b = np.random.default_rng(0).uniform(-1, 1, (a.n_cols, 128)).astype(np.float32)
+    c = P.hybrid_spmm(m, P.DenseMatrix.from_array(b), P.ExecConfig(math="tf32")).data
+    _, ref64 = O.spmm_f64(O.Csr.of(a), b)
+    assert O.rel_frobenius(c, ref64) <= TF32_TOL
+    with pytest.raises(ValueError):
+        P.hybrid_spmm(m, P.DenseMatrix.from_array(b[:, :100]), P.ExecConfig(math="tf32"))

@@ -42,7 +42,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 template <int KIND>  // 0 = tf32, 1 = bf16
-__global__ void probe(const float* G, const float* Blk, float* D, int reps, long long* cycles) {
+__global__ void probe(const float* G, const float* Blk, float* D, int reps, long long* cycles, int rot) {
   // G: [KB][128] fp32 (KB = 8 tf32 / 16 bf16 gathered rows); Blk: [8][KB] fp32 (dense block rows)
   constexpr int KB = KIND == 0 ? 8 : 16;
   constexpr int EB = KIND == 0 ? 4 : 2;
@@ -57,10 +57,16 @@ __global__ void probe(const float* G, const float* Blk, float* D, int reps, long
   for (int idx = tid; idx < KB * 128; idx += blockDim.x) {
     int k = idx / 128, f = idx % 128;
     int ma = f / per_atom_f, fi = f % per_atom_f;
-    int kg = k / 8, kr = k % 8;
     int byte = fi * EB;
     int chunk = byte >> 4, within = byte & 15;
-    int off = (kg * n_mn_atoms + ma) * 1024 + kr * 128 + ((chunk ^ kr) << 4) + within;
+    int off;
+    if (KIND == 0) {  // SWIZZLE_128B_BASE32B: atom = 4 K-rows x 128 B, 32-B granules XOR row
+      int kg = k / 4, kr = k % 4;
+      off = kg * 2048 + ma * 512 + kr * 128 + ((((chunk >> 1) ^ kr)) << 5) + ((chunk & 1) << 4) + within;
+    } else {          // SWIZZLE_128B: atom = 8 K-rows x 128 B, 16-B chunks XOR row
+      int kg = k / 8, kr = k % 8;
+      off = kg * 2048 + ma * 1024 + kr * 128 + ((chunk ^ kr) << 4) + within;
+    }
     if (KIND == 0) *(float*)(sA + off) = G[k * 128 + f];
     else *(__nv_bfloat16*)(sA + off) = __float2bfloat16(G[k * 128 + f]);
   }
@@ -76,7 +82,7 @@ __global__ void probe(const float* G, const float* Blk, float* D, int reps, long
   asm volatile("fence.proxy.async.shared::cta;");
   if (tid == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(&tmem_base)), "r"(32));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(&tmem_base)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -86,19 +92,21 @@ __global__ void probe(const float* G, const float* Blk, float* D, int reps, long
   // descriptors
   uint32_t idesc = (1u << 4) | ((KIND == 0 ? 2u : 1u) << 7) | ((KIND == 0 ? 2u : 1u) << 10) | (1u << 15) | (0u << 16) |
                    ((8u >> 3) << 17) | ((128u >> 4) << 24);
-  uint64_t adesc = desc_sw128_mn(smem_u32(sA), 1024, n_mn_atoms * 1024);
+  uint64_t adesc = KIND == 0 ? (desc_none(smem_u32(sA), 512, 2048) | ((uint64_t)1 << 61))
+                             : desc_sw128_mn(smem_u32(sA), 1024, 2048);
   uint64_t bdesc = desc_none(smem_u32(sB), 128, 256);
   long long t0 = 0, t1 = 0;
   if (tid == 0) {
     t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-      uint32_t acc = r > 0;
+      uint32_t acc = r >= rot;
+      uint32_t dcol = tmem + (uint32_t)((r % rot) * 8);
       if (KIND == 0)
         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}"
-                     :: "r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+                     :: "r"(dcol), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
       else
         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}"
-                     :: "r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+                     :: "r"(dcol), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(&bar)));
     mbar_wait(&bar, 0);
@@ -120,7 +128,7 @@ __global__ void probe(const float* G, const float* Blk, float* D, int reps, long
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(32));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
 }
 
 static float tf32_trunc(float x) { uint32_t u; memcpy(&u, &x, 4); u &= 0xFFFFE000u; memcpy(&x, &u, 4); return x; }
@@ -142,7 +150,7 @@ void run(const char* name) {
   CK(cudaMalloc(&dG, G.size() * 4)); CK(cudaMalloc(&dB, Blk.size() * 4)); CK(cudaMalloc(&dD, D.size() * 4)); CK(cudaMalloc(&dc, 8));
   CK(cudaMemcpy(dG, G.data(), G.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, Blk.data(), Blk.size() * 4, cudaMemcpyHostToDevice));
-  probe<KIND><<<1, 128>>>(dG, dB, dD, 1, dc);
+  probe<KIND><<<1, 128>>>(dG, dB, dD, 1, dc, 1);
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
   double max_err = 0, max_ref = 0, max_err_tr = 0;
@@ -161,11 +169,12 @@ void run(const char* name) {
     }
   printf("%s layout check: max|D-ref| %.3e (vs quantized-operand ref %.3e), max|ref| %.3f, D[0][0]=%.9f (1+3/4096 -> trunc 1.0, RN %.9f)\n",
          name, max_err, max_err_tr, max_ref, D[0], 1.0 + 1.0 / 1024);
-  for (int reps : {1000, 10000}) {
-    probe<KIND><<<1, 128>>>(dG, dB, dD, reps, dc);
+  for (int rot : {1, 4, 16, 64}) {
+    int reps = 8192;
+    probe<KIND><<<1, 128>>>(dG, dB, dD, reps, dc, rot);
     CK(cudaDeviceSynchronize());
     long long c; CK(cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost));
-    printf("%s throughput: %d MMAs (M=128,N=8,K=%d) in %lld cycles = %.2f cyc/MMA\n", name, reps, KB, c, (double)c / reps);
+    printf("%s throughput: %d MMAs (M=128,N=8,K=%d) over %d accumulators in %lld cycles = %.2f cyc/MMA\n", name, reps, KB, rot, c, (double)c / reps);
   }
 }
 

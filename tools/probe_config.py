@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--workload", default="rmat1m")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--math", default="auto")
+    ap.add_argument("--l1", type=int, default=1)
     args = ap.parse_args()
     t0 = time.time()
     a = synth.workload_matrix(args.workload)
@@ -49,20 +51,20 @@ def main():
     out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(3):
-        spmm_device(t, bt, out=out)
+        spmm_device(t, bt, out=out, math=args.math, l1=bool(args.l1))
     torch.cuda.synchronize()
     times = []
     for _ in range(args.iters):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        spmm_device(t, bt, out=out)
+        spmm_device(t, bt, out=out, math=args.math, l1=bool(args.l1))
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     ms = float(np.median(times))
     flops = 2.0 * a.nnz * b.shape[1]
-    print(f"spmm_cc median {ms:.3f} ms  min {min(times):.3f}  -> {flops / ms / 1e6:.1f} GFLOP/s", flush=True)
+    print(f"spmm[{args.math}, l1={args.l1}] median {ms:.3f} ms  min {min(times):.3f}  -> {flops / ms / 1e6:.1f} GFLOP/s", flush=True)
     if args.check:
         import oracle as O
         c = out.cpu().numpy()
@@ -72,7 +74,7 @@ def main():
         errs = []
         for lo in range(0, len(rows), 1):
             pass
-        ref32, ref64 = O.spmm_f64(oc, b)
+        ref32, ref64 = O.spmm_f64(oc, bt.float().cpu().numpy())
         print("max_rel", O.max_relative_error(c, ref32), "relF", O.rel_frobenius(c, ref64), flush=True)
 
 

@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--math", default="auto", choices=["auto", "fp32", "tf32"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -243,9 +244,15 @@ def run_single(args):
     alg_bytes, touched = algorithmic_bytes(a, w.n_features, b_elem, 2 if w.dtype == "bf16" else 4)
     flops = 2.0 * a.nnz * w.n_features
 
-    # preprocessing on device (reported separately from the steady-state SpMM)
+    # preprocessing on device (reported separately from the steady-state SpMM); the first build
+    # also pays one-time library / allocator initialisation, so the second one is reported
     d = DeviceCsr.from_host(a, dev)
     torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tile = build_device(d)
+    torch.cuda.synchronize()
+    t_build_first = time.perf_counter() - t0
+    del tile
     t0 = time.perf_counter()
     tile = build_device(d)
     torch.cuda.synchronize()
@@ -260,11 +267,31 @@ def run_single(args):
     out = torch.empty((a.n_rows, w.n_features), dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream()
 
+    # arithmetic path: fp32 B -> exact FP32 (CUDA cores) or TF32 (tensor cores); bf16 B -> tensor
+    # cores when the shape allows.  "auto" times both for a few launches and keeps the faster.
+    from paper_2603_08734_b200.device import resolve_math, tc_eligible
+    candidates = ["fp32", "tf32"] if (w.dtype == "f32" and tc_eligible(tile, bt)) else ["auto"]
+    if args.math != "auto":
+        candidates = [args.math]
+    path_ms = {}
+    for m in candidates:
+        for _ in range(2):
+            spmm_device(tile, bt, out=out, math=m)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(5):
+            spmm_device(tile, bt, out=out, math=m)
+        e1.record(st)
+        torch.cuda.synchronize()
+        path_ms[m] = e0.elapsed_time(e1) / 5
+    math = min(path_ms, key=path_ms.get)
+    kernel = "k_spmm_tc" if resolve_math(math, bt, tile, "f32") == "tc" else "k_spmm_cc"
+
     clocks = ClockSampler(0)
     clocks.start()
     time.sleep(0.3)
     for _ in range(args.warmup):
-        spmm_device(tile, bt, out=out)
+        spmm_device(tile, bt, out=out, math=math)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -273,7 +300,7 @@ def run_single(args):
     g0.record(st)
     for e0, e1 in ev:
         e0.record(st)
-        spmm_device(tile, bt, out=out)
+        spmm_device(tile, bt, out=out, math=math)
         e1.record(st)
     g1.record(st)
     torch.cuda.synchronize()
@@ -310,7 +337,7 @@ def run_single(args):
         for k, v in host.items():
             dev_bufs[k].copy_(v, non_blocking=True)
         b_dev2.copy_(b_host, non_blocking=True)
-        spmm_device(t2, b_dev2, out=out)
+        spmm_device(t2, b_dev2, out=out, math=math)
         c_host.copy_(out, non_blocking=True)
         s1.record(st)
         torch.cuda.synchronize()
@@ -326,27 +353,28 @@ def run_single(args):
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else "f32",
+        "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else ("tf32" if math == "tf32" else "f32"),
         "data": "synthetic",
         "config": {"workload": args.workload, "description": w.description, "n_rows": a.n_rows,
                    "n_cols": a.n_cols, "nnz": a.nnz, "n_features": w.n_features,
-                   "parallelism": "single GPU", "math": "fp32 CUDA-core FMA" if w.dtype == "f32" else
-                   "bf16 B, fp32 FMA", "l2": "no flush: per-step inputs (A + B + C = "
+                   "parallelism": "single GPU", "math": math, "kernel": kernel,
+                   "path_ms": path_ms, "l2": "no flush: per-step inputs (A + B + C = "
                    f"{(alg_bytes + gathered * 0) / 1e9:.2f} GB compulsory) exceed the 126 MB L2",
-                   "preprocess_ms": {"build_device": 1e3 * t_build, "schedule": 1e3 * t_sched},
+                   "preprocess_ms": {"build_device": 1e3 * t_build, "build_device_first_call": 1e3 * t_build_first,
+                                     "schedule": 1e3 * t_sched},
                    "format": {"entries": tile.n_entries, "blocks": tile.n_blocks, "residual_rows": tile.n_res,
                               "units": plan.units, "uncovered_rows": plan.uncovered}},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(args.workload),
-                     "algorithmic_bytes": alg_bytes, "kernel": "k_spmm_cc", "kernel_ms": kern_avg,
+                     "algorithmic_bytes": alg_bytes, "kernel": kernel, "kernel_ms": kern_avg,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
         "gather": {"gathered_bytes": gathered, "achieved_gbs": gathered / (kern_avg * 1e-3) / 1e9,
                    "roof_gbs": GATHER_ROOF_GBS,
                    "frac": gathered / (kern_avg * 1e-3) / 1e9 / GATHER_ROOF_GBS},
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms)),
-                "path": "rsh_spmm_cc via ctypes, pinned host format + B in, C out"},
+                "path": f"{kernel} via the C ABI (ctypes), pinned host format + B in, C out"},
         "cpu_baseline": cpu,
         "clocks": clk,
     }

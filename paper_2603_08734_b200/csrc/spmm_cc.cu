@@ -107,73 +107,6 @@ __global__ void k_tail_units(Sched s, int64_t n_res) {
 // the persistent CUDA-core kernel: one warp per work unit, units fetched dynamically
 // ------------------------------------------------------------------------------------------
 
-// fp32 window chunk with all gathers of a block in flight at once: the B rows of the (up to 8)
-// occupied column slots are loaded into registers first (predicated, statically indexed), then
-// the set bits are consumed in bit order -- row i unrolled, column j dispatched by a switch so
-// both the accumulator row and the B-row register stay static.  The next block's metadata
-// (bitmap, col ids, packed values) is fetched before the current block is multiplied.
-template <int VEC, class BT>
-__device__ __forceinline__ void window_chunk_f32(const SpmmArgs& a, int32_t b0, int32_t b1, int f0, bool active,
-                                                 float (&acc)[8][VEC]) {
-  const int lane = threadIdx.x & 31;
-  const BT* B = reinterpret_cast<const BT*>(a.B);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int t = 0; t < VEC; ++t) acc[i][t] = 0.f;
-  if (b0 >= b1) return;
-  auto meta = [&](int32_t blk, unsigned long long& bm, int32_t& colreg, float& v0, float& v1) {
-    bm = __ldg(a.bitmaps + blk);
-    colreg = lane < 8 ? __ldg(a.col_id + (int64_t)blk * 8 + lane) : 0;
-    const int32_t vs = __ldg(a.s.vstart + blk);
-    const int nv = __popcll(bm);
-    v0 = lane < nv ? __ldg(a.tc_values + vs + lane) : 0.f;
-    v1 = lane + 32 < nv ? __ldg(a.tc_values + vs + 32 + lane) : 0.f;
-  };
-  unsigned long long bm;
-  int32_t colreg;
-  float v0, v1;
-  meta(b0, bm, colreg, v0, v1);
-  for (int32_t blk = b0; blk < b1; ++blk) {
-    unsigned long long x = bm | (bm >> 32);
-    x |= x >> 16;
-    x |= x >> 8;
-    const uint32_t cm = (uint32_t)x & 0xffu;
-    float bv[8][VEC];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int32_t c = __shfl_sync(0xffffffffu, colreg, j);
-      if (active && ((cm >> j) & 1u)) load_vec<VEC, BT>(B + (int64_t)c * a.ldb + f0, bv[j]);
-    }
-    const unsigned long long cbm = bm;
-    const float cv0 = v0, cv1 = v1;
-    if (blk + 1 < b1) meta(blk + 1, bm, colreg, v0, v1);
-    int kk = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      uint32_t rb = uint32_t(cbm >> (8 * i)) & 0xffu;
-      while (rb) {
-        const int j = __ffs(rb) - 1;
-        rb &= rb - 1;
-        const float va = __shfl_sync(0xffffffffu, cv0, kk & 31);
-        const float vb = __shfl_sync(0xffffffffu, cv1, kk & 31);
-        const float v = kk < 32 ? va : vb;
-        ++kk;
-        if (active) {
-          switch (j) {
-#define RSH_CASE(J)                                                             \
-  case J:                                                                       \
-    _Pragma("unroll") for (int t = 0; t < VEC; ++t) acc[i][t] = fmaf(v, bv[J][t], acc[i][t]); \
-    break;
-            RSH_CASE(0) RSH_CASE(1) RSH_CASE(2) RSH_CASE(3) RSH_CASE(4) RSH_CASE(5) RSH_CASE(6) RSH_CASE(7)
-#undef RSH_CASE
-          }
-        }
-      }
-    }
-  }
-}
-
 template <int VEC, class BT, class AccT>
 __device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int32_t b1, int f0, bool active,
                                              AccT (&acc)[8][VEC]) {
@@ -236,10 +169,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm_cc(SpmmArgs a) {
         int f0 = fc * 32 * VEC + lane * VEC;
         bool active = f0 < a.N;
         AccT acc[8][VEC];
-        if constexpr (std::is_same<AccT, float>::value)
-          window_chunk_f32<VEC, BT>(a, un.z, un.w, f0, active, acc);
-        else
-          window_chunk<VEC, BT, AccT>(a, un.z, un.w, f0, active, acc);
+        window_chunk<VEC, BT, AccT>(a, un.z, un.w, f0, active, acc);
         if (slot < 0) {
           if (active) {
 #pragma unroll

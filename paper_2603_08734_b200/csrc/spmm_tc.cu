@@ -12,23 +12,27 @@
 // Warp roles per CTA (one CTA per SM, persistent, cost-balanced contiguous unit ranges):
 //   warps 0-3   epilogue: tcgen05.ld -> registers -> streaming C stores (or chunk partials +
 //               ordered ticket reduction for windows longer than kChunk blocks)
-//   warps 4-7   MMA issuers (one lane each, one per SM sub-partition) + TMEM allocation
-//   warps 8-19  producers: block metadata, gather, decode, mbarrier signalling; afterwards they
-//               take the residual / zero-row units (CUDA-core path) from a global counter.
+//   warps 4-7   MMA issuers, one per pipeline / SM sub-partition (+ TMEM allocation)
+//   warps 8-19  producers, 3 per pipeline: block metadata, gather, decode, mbarrier signalling;
+//               afterwards they take the residual / zero-row units (CUDA-core path) from a
+//               global counter.
+// Units ua = w (mod 4) of the CTA's range form pipeline w with its own stage ring, consumed
+// strictly in order; the epilogue drains accumulators in unit order.
 #include "sched.cuh"
 
 namespace rsh {
 namespace tc {
 
+constexpr int kPipes = 4;        // independent producer -> MMA pipelines per CTA
+constexpr int kProdPerPipe = 3;  // producer warps per pipeline
 constexpr int kEpiWarps = 4;
 constexpr int kMmaWarp0 = 4;
-constexpr int kMmaWarps = 4;
+constexpr int kMmaWarps = kPipes;
 constexpr int kProd0 = kMmaWarp0 + kMmaWarps;
-constexpr int kProdWarps = 12;
+constexpr int kProdWarps = kPipes * kProdPerPipe;
 constexpr int kThreadsTC = (kProd0 + kProdWarps) * 32;
 constexpr int kTileBytes = 4096;  // A operand bytes per 128-feature tile per block
 constexpr int kBopBytes = 256;    // decoded block (8 rows x 32 B)
-constexpr int kRawBytes = 256;    // packed values of one block (<= 64 floats)
 constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -39,13 +43,21 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n.reg .pred p;\nRSH_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra RSH_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Bounded wait: a protocol bug traps (the launch fails with an error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (uint32_t n = 0; !mbar_try(bar, parity); ++n)
+    if (n == (1u << 26)) __trap();
 }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -134,17 +146,19 @@ __device__ __forceinline__ int64_t cost_bound(const int64_t* __restrict__ cost, 
   return lo;
 }
 
-template <class BT, int MT, int STAGES, int DEPTH, bool kL1>
+template <class BT, int MT, int STAGES, bool kL1>
 __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
   constexpr int EB = Kind<BT>::eb;
   constexpr int NACC = kTmemCols / (8 * MT) < 64 ? kTmemCols / (8 * MT) : 64;
   constexpr int kVec = 4 * MT;  // per-lane features (N = 128 MT) for the CUDA-core tail units
+  constexpr int SP = STAGES / kPipes;  // stages per pipeline
+  static_assert(STAGES % kPipes == 0, "stages split evenly across pipelines");
+  static_assert(SP >= 2, "at least double buffering per pipeline");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                                   // STAGES * MT * 4 KB
   uint8_t* sB = sA + STAGES * MT * kTileBytes;          // STAGES * 256 B decoded blocks
-  uint8_t* sRaw = sB + STAGES * kBopBytes;              // STAGES * 256 B packed values
-  uint64_t* full = (uint64_t*)(sRaw + STAGES * kRawBytes);
+  uint64_t* full = (uint64_t*)(sB + STAGES * kBopBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + NACC;
@@ -158,7 +172,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, 33);  // 32 lanes' cp.async completions (noinc) + the decode arrive
       mbar_init(empty + s, 1);
     }
     for (int s = 0; s < NACC; ++s) {
@@ -186,76 +200,78 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
 
   if (warp >= kProd0) {
     // ---------------------------------------------------------------- producers
-    // The CTA's window units cover one contiguous block range [B0, B1) (units are consecutive
-    // chunks of consecutive entries), consumed by the MMA warp in order j = blk - B0.  Producer
-    // p owns blocks B0 + p + P*i.  Metadata (bitmap, value start, 8 col ids) for 32 of its blocks
-    // is fetched in one coalesced batch (lane l <-> block l); per block the warp then only issues
-    // asynchronous copies -- 8 gathered B rows (16 B per lane per row, zero-filled for padding
-    // slots) and the packed values -- and decodes the block DEPTH blocks later, once its copies
-    // have landed, so no global-memory latency sits on the per-block path.
-    const int p = warp - kProd0;
+    // Pipeline w (of kPipes) owns the units ua = w (mod kPipes) of this CTA, in order, and its own
+    // ring of SP stages; its kProdPerPipe producer warps split the pipeline's block sequence
+    // m = 0, 1, 2, ... round robin.  Unit metadata (bitmap, value start, 8 col ids of each of
+    // its <= kChunk blocks; lane l <-> block l) is fetched one unit ahead in one coalesced load;
+    // block values are prefetched two blocks ahead into registers.  Per block the warp then only
+    // waits for a free stage, issues the 8 row gathers (cp.async, 16 B per lane per row,
+    // zero-filled for padding slots) whose completion the hardware reports on the stage's full
+    // barrier (cp.async.mbarrier.arrive.noinc), and decodes the bitmap block into the MMA B
+    // operand.  No global-memory latency sits on the per-block path, and every stage of the
+    // ring can be in flight.  Consumption is in order per pipeline, which keeps the mbarrier
+    // parity protocol exact.
+    const int pw = warp - kProd0;
+    const int w = pw / kProdPerPipe, q = pw % kProdPerPipe;
     const char* Bbytes = reinterpret_cast<const char*>(a.B);
     const int64_t row_bytes = a.ldb * EB;
-    const int64_t B0 = u0 < u1 ? a.s.units[u0].z : 0;
-    const int64_t B1 = u0 < u1 ? a.s.units[u1 - 1].w : 0;
-    int64_t pj[DEPTH + 1];
-    unsigned long long pb[DEPTH + 1];
-    int npend = 0;
-    auto complete = [&](int64_t jo, unsigned long long bmo) {
-      const int so = (int)(jo % STAGES);
-      const float* raw = reinterpret_cast<const float*>(sRaw + (size_t)so * kRawBytes);
-      uint8_t* bop = sB + (size_t)so * kBopBytes;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int pos = lane + 32 * h;
-        const bool set = (bmo >> pos) & 1ull;
-        const int rank = pos ? __popcll(bmo & ((1ull << pos) - 1ull)) : 0;
-        const float v = set ? raw[rank] : 0.f;
-        const int i = pos >> 3, k = pos & 7;
-        if constexpr (EB == 4) {
-          *(uint32_t*)(bop + (k >> 2) * 128 + i * 16 + (k & 3) * 4) = to_tf32(v);
-        } else if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
-          *(__nv_bfloat16*)(bop + i * 16 + k * 2) = __float2bfloat16_rn(v);
-        } else {
-          *(__half*)(bop + i * 16 + k * 2) = __float2half_rn(v);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(full + so);
+    struct Meta {
+      unsigned long long bm;
+      int32_t vs;
+      int4 c0, c1;
+      int32_t z, nb;
     };
-    for (int64_t base = B0 + p; base < B1; base += 32 * kProdWarps) {
-      const int64_t myblk = base + (int64_t)kProdWarps * lane;
-      const bool mine = myblk < B1;
-      const unsigned long long mbm = mine ? __ldg(a.bitmaps + myblk) : 0ull;
-      const int32_t mvs = mine ? __ldg(a.s.vstart + myblk) : 0;
-      int4 mc0 = make_int4(0, 0, 0, 0), mc1 = make_int4(0, 0, 0, 0);
-      if (mine) {
-        mc0 = __ldg(reinterpret_cast<const int4*>(a.col_id + myblk * 8));
-        mc1 = __ldg(reinterpret_cast<const int4*>(a.col_id + myblk * 8) + 1);
-      }
-      const int64_t left = (B1 - base + kProdWarps - 1) / kProdWarps;
-      const int nbatch = left < 32 ? (int)left : 32;
-      for (int l = 0; l < nbatch; ++l) {
-        const int64_t blk = base + (int64_t)kProdWarps * l;
-        const int64_t jj = blk - B0;
-        const int s = (int)(jj % STAGES);
-        const unsigned long long bm = __shfl_sync(0xffffffffu, mbm, l);
-        const int32_t vs = __shfl_sync(0xffffffffu, mvs, l);
+    auto load_meta = [&](int64_t u, Meta& M) {
+      const int4 un = a.s.units[u];
+      M.z = un.z;
+      M.nb = un.w - un.z;
+      const int64_t blk = (int64_t)un.z + lane;
+      const bool mine = lane < M.nb;
+      M.bm = mine ? __ldg(a.bitmaps + blk) : 0ull;
+      M.vs = mine ? __ldg(a.s.vstart + blk) : 0;
+      M.c0 = mine ? __ldg(reinterpret_cast<const int4*>(a.col_id + blk * 8)) : make_int4(0, 0, 0, 0);
+      M.c1 = mine ? __ldg(reinterpret_cast<const int4*>(a.col_id + blk * 8) + 1) : make_int4(0, 0, 0, 0);
+    };
+    auto load_vals = [&](const Meta& M, int l, float& v0, float& v1) {
+      const unsigned long long bm = __shfl_sync(0xffffffffu, M.bm, l);
+      const int32_t vs = __shfl_sync(0xffffffffu, M.vs, l);
+      const int nv = __popcll(bm);
+      v0 = lane < nv ? __ldg(a.tc_values + vs + lane) : 0.f;
+      v1 = lane + 32 < nv ? __ldg(a.tc_values + vs + 32 + lane) : 0.f;
+    };
+    Meta cur, nxt;
+    int64_t u = u0 + w;
+    if (u < u1) load_meta(u, cur);
+    int64_t m0 = 0;  // pipeline block count before the current unit
+    for (; u < u1; u += kPipes) {
+      if (u + kPipes < u1) load_meta(u + kPipes, nxt);
+      const int nb = cur.nb;
+      const int first = (int)(((q - m0) % kProdPerPipe + kProdPerPipe) % kProdPerPipe);
+      float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f;  // values of the next two blocks
+      if (first < nb) load_vals(cur, first, pa0, pa1);
+      if (first + kProdPerPipe < nb) load_vals(cur, first + kProdPerPipe, pb0, pb1);
+      for (int l = first; l < nb; l += kProdPerPipe) {
+        const float v0 = pa0, v1 = pa1;
+        pa0 = pb0;
+        pa1 = pb1;
+        if (l + 2 * kProdPerPipe < nb) load_vals(cur, l + 2 * kProdPerPipe, pb0, pb1);
+        const int64_t m = m0 + l;
+        const int s = w * SP + (int)(m % SP);
+        const unsigned long long bm = __shfl_sync(0xffffffffu, cur.bm, l);
         int32_t col[8];
-        col[0] = __shfl_sync(0xffffffffu, mc0.x, l);
-        col[1] = __shfl_sync(0xffffffffu, mc0.y, l);
-        col[2] = __shfl_sync(0xffffffffu, mc0.z, l);
-        col[3] = __shfl_sync(0xffffffffu, mc0.w, l);
-        col[4] = __shfl_sync(0xffffffffu, mc1.x, l);
-        col[5] = __shfl_sync(0xffffffffu, mc1.y, l);
-        col[6] = __shfl_sync(0xffffffffu, mc1.z, l);
-        col[7] = __shfl_sync(0xffffffffu, mc1.w, l);
+        col[0] = __shfl_sync(0xffffffffu, cur.c0.x, l);
+        col[1] = __shfl_sync(0xffffffffu, cur.c0.y, l);
+        col[2] = __shfl_sync(0xffffffffu, cur.c0.z, l);
+        col[3] = __shfl_sync(0xffffffffu, cur.c0.w, l);
+        col[4] = __shfl_sync(0xffffffffu, cur.c1.x, l);
+        col[5] = __shfl_sync(0xffffffffu, cur.c1.y, l);
+        col[6] = __shfl_sync(0xffffffffu, cur.c1.z, l);
+        col[7] = __shfl_sync(0xffffffffu, cur.c1.w, l);
         unsigned long long x = bm | (bm >> 32);
         x |= x >> 16;
         x |= x >> 8;
         const uint32_t cm = (uint32_t)x & 0xffu;
-        mbar_wait(empty + s, (uint32_t)(((jj / STAGES) & 1) ^ 1));
+        mbar_wait(empty + s, (uint32_t)(((m / SP) & 1) ^ 1));
         const uint32_t stageA = smem_u32(sA + (size_t)s * MT * kTileBytes);
         constexpr int kChunksPerTileRow = 8 * EB;  // 16-B chunks of 128 features
         constexpr int kChunksPerRow = MT * kChunksPerTileRow;
@@ -271,41 +287,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
             cp16<kL1>(dst, src_row + cc * 16, nbytes);
           }
         }
-        // packed values of the block -> raw slot (bit order)
-        const int nv = __popcll(bm);
-        const uint32_t rawdst = smem_u32(sRaw + (size_t)s * kRawBytes);
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
+        // decode: bit pos = local_row * 8 + local_col, value rank = popc(bits below pos)
+        uint8_t* bop = sB + (size_t)s * kBopBytes;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int q = lane + 32 * h;
-          if (q < nv)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rawdst + q * 4), "l"(a.tc_values + vs + q)
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-#pragma unroll
-        for (int z = 0; z <= DEPTH; ++z)
-          if (z == npend) {
-            pj[z] = jj;
-            pb[z] = bm;
+          const int pos = lane + 32 * h;
+          const bool set = (bm >> pos) & 1ull;
+          const int rank = pos ? __popcll(bm & ((1ull << pos) - 1ull)) : 0;
+          const float va = __shfl_sync(0xffffffffu, v0, rank & 31);
+          const float vb = __shfl_sync(0xffffffffu, v1, rank & 31);
+          const float v = set ? (rank < 32 ? va : vb) : 0.f;
+          const int i = pos >> 3, k = pos & 7;
+          if constexpr (EB == 4) {
+            *(uint32_t*)(bop + (k >> 2) * 128 + i * 16 + (k & 3) * 4) = to_tf32(v);
+          } else if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
+            *(__nv_bfloat16*)(bop + i * 16 + k * 2) = __float2bfloat16_rn(v);
+          } else {
+            *(__half*)(bop + i * 16 + k * 2) = __float2half_rn(v);
           }
-        if (++npend > DEPTH) {
-          asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH) : "memory");
-          __syncwarp();
-          complete(pj[0], pb[0]);
-#pragma unroll
-          for (int z = 0; z < DEPTH; ++z) {
-            pj[z] = pj[z + 1];
-            pb[z] = pb[z + 1];
-          }
-          --npend;
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(full + s);
       }
+      m0 += nb;
+      cur = nxt;
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
-#pragma unroll
-    for (int z = 0; z < DEPTH; ++z)
-      if (z < npend) complete(pj[z], pb[z]);
+    asm volatile("cp.async.wait_all;" ::: "memory");
 
     // residual and zero-row units (CUDA-core), fetched dynamically across the grid
     const int64_t nunits = a.s.header[2];
@@ -330,17 +339,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
     }
   } else if (warp >= kMmaWarp0) {
     // ---------------------------------------------------------------- MMA issuers
-    // One elected lane per warp; a tiny M=128 x N=8 MMA costs ~200 cycles of issue latency per
-    // thread (tools/microbench/umma_issue.cu), so four warps (one per SM sub-partition) issue
-    // in parallel, warp w taking the units ua = w (mod 4), each into its own accumulator.
+    // One elected lane per pipeline.  A tiny M=128 x N=8 MMA costs ~200 cycles of issue latency
+    // per issuing thread and the rate scales with issuing warps (tools/microbench/umma_issue.cu),
+    // so each of the kPipes pipelines has its own issuer, in its own SM sub-partition, consuming
+    // its stage ring strictly in order into its own accumulators.
     if (lane == 0) {
       constexpr uint32_t idesc = (1u << 4) | (Kind<BT>::fmt << 7) | (Kind<BT>::fmt << 10) | (1u << 15) |
                                  (1u << 17) | (8u << 24);
-      const int mw = warp - kMmaWarp0;
-      const int64_t B0 = u0 < u1 ? a.s.units[u0].z : 0;
-      int64_t ua = mw;
-      for (int64_t u = u0 + mw; u < u1; u += kMmaWarps, ua += kMmaWarps) {
-        int4 un = a.s.units[u];
+      const int w = warp - kMmaWarp0;
+      int64_t m = 0;
+      int64_t ua = w;
+      for (int64_t u = u0 + w; u < u1; u += kPipes, ua += kPipes) {
+        const int4 un = a.s.units[u];
         const int slot = (int)(ua % NACC);
         mbar_wait(tempty + slot, (uint32_t)(((ua / NACC) & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -348,10 +358,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
           mbar_arrive(tfull + slot);
           continue;
         }
-        int64_t j = un.z - B0;
-        for (int32_t blk = un.z; blk < un.w; ++blk, ++j) {
-          const int s = (int)(j % STAGES);
-          mbar_wait(full + s, (uint32_t)((j / STAGES) & 1));
+        for (int32_t blk = un.z; blk < un.w; ++blk, ++m) {
+          const int s = w * SP + (int)(m % SP);
+          mbar_wait(full + s, (uint32_t)((m / SP) & 1));
+          // the gathered rows were written by cp.async (generic proxy) and observed through
+          // the barrier; make them visible to the tensor core's async-proxy operand reads
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t bdesc = umma_desc(smem_u32(sB + (size_t)s * kBopBytes), 128, 256, 0);
 #pragma unroll
@@ -451,12 +463,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
 template <int MT, int STAGES>
 constexpr size_t smem_bytes() {
   constexpr int NACC = kTmemCols / (8 * MT) < 64 ? kTmemCols / (8 * MT) : 64;
-  return 1024 + (size_t)STAGES * (MT * kTileBytes + kBopBytes + kRawBytes) + (2 * STAGES + 2 * NACC) * 8 + 16;
+  return 1024 + (size_t)STAGES * (MT * kTileBytes + kBopBytes) + (2 * STAGES + 2 * NACC) * 8 + 16;
 }
 
-template <class BT, int MT, int STAGES, int DEPTH, bool kL1>
+template <class BT, int MT, int STAGES, bool kL1>
 int launch(const SpmmArgs& a, cudaStream_t st) {
-  auto kern = k_spmm_tc<BT, MT, STAGES, DEPTH, kL1>;
+  auto kern = k_spmm_tc<BT, MT, STAGES, kL1>;
   constexpr size_t bytes = smem_bytes<MT, STAGES>();
   static bool init = false;
   if (!init) {
@@ -510,15 +522,15 @@ int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.partials = partials;
   const int mt = (int)(N / 128);
   if (b_dtype == 0) {
-    if (mt == 1) return l1 ? tc::launch<float, 1, 40, 3, true>(a, st) : tc::launch<float, 1, 40, 3, false>(a, st);
-    return l1 ? tc::launch<float, 2, 20, 1, true>(a, st) : tc::launch<float, 2, 20, 1, false>(a, st);
+    if (mt == 1) return l1 ? tc::launch<float, 1, 48, true>(a, st) : tc::launch<float, 1, 48, false>(a, st);
+    return l1 ? tc::launch<float, 2, 24, true>(a, st) : tc::launch<float, 2, 24, false>(a, st);
   }
   if (b_dtype == 1) {
-    if (mt == 1) return l1 ? tc::launch<__nv_bfloat16, 1, 40, 3, true>(a, st) : tc::launch<__nv_bfloat16, 1, 40, 3, false>(a, st);
-    return l1 ? tc::launch<__nv_bfloat16, 2, 20, 1, true>(a, st) : tc::launch<__nv_bfloat16, 2, 20, 1, false>(a, st);
+    if (mt == 1) return l1 ? tc::launch<__nv_bfloat16, 1, 48, true>(a, st) : tc::launch<__nv_bfloat16, 1, 48, false>(a, st);
+    return l1 ? tc::launch<__nv_bfloat16, 2, 24, true>(a, st) : tc::launch<__nv_bfloat16, 2, 24, false>(a, st);
   }
-  if (mt == 1) return l1 ? tc::launch<__half, 1, 40, 3, true>(a, st) : tc::launch<__half, 1, 40, 3, false>(a, st);
-  return l1 ? tc::launch<__half, 2, 20, 1, true>(a, st) : tc::launch<__half, 2, 20, 1, false>(a, st);
+  if (mt == 1) return l1 ? tc::launch<__half, 1, 48, true>(a, st) : tc::launch<__half, 1, 48, false>(a, st);
+  return l1 ? tc::launch<__half, 2, 24, true>(a, st) : tc::launch<__half, 2, 24, false>(a, st);
 }
 
 }  // extern "C"

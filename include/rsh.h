@@ -77,13 +77,15 @@ int rsh_residual_gather(const int64_t* row_ptr, const int32_t* col_idx, const fl
                         float* res_values, cudaStream_t stream);
 
 /* ---- persistent-kernel schedule: execute.py:136-168 (_window_groups, value starts) as device
- *      data.  header_out (device int64[8], may be NULL) = [groups, window units, units,
- *      partial slots, uncovered rows, 0, 0, 0]. ------------------------------------------- */
+ *      data.  Logical windows are cut into units of chunk_blocks blocks (>= 32; rsh_spmm_cc is
+ *      tuned for 32, rsh_spmm_tc for 256) at fixed offsets, so results never depend on the
+ *      format's split segments.  header_out (device int64[8], may be NULL) = [groups, window
+ *      units, units, partial slots, uncovered rows, chunk_blocks, 0, 0]. ------------------- */
 size_t rsh_schedule_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res);
 int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_id,
                  const int64_t* row_window_offset, int64_t n_entries, const uint64_t* bitmaps, int64_t n_blocks,
-                 const int32_t* res_row_id, int64_t n_res, void* sched, size_t sched_bytes, int64_t* header_out,
-                 cudaStream_t stream);
+                 const int32_t* res_row_id, int64_t n_res, int32_t chunk_blocks, void* sched, size_t sched_bytes,
+                 int64_t* header_out, cudaStream_t stream);
 size_t rsh_partials_bytes(int64_t partial_slots, int64_t n_features, int32_t accum);
 
 /* ---- hybrid SpMM: execute.py:155-218 hybrid_spmm.  C[n_rows x N] (row stride ldc) is
@@ -105,6 +107,10 @@ int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 const int64_t* res_offset, const int32_t* res_col_id, const float* res_values, int64_t n_res,
                 const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t l1,
                 void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
+
+/* debug: per-CTA role cycle counters of the last rsh_spmm_tc launches run with l1 bit 4 set
+ * (host_out: 1024 x 16 uint64), cleared after reading */
+int rsh_tc_profile(unsigned long long* host_out);
 
 /* ---- verification: core.py:398-408 max_relative_error, result in out[0] (device double) - */
 int rsh_max_relative_error(const float* c, const float* ref, int64_t rows, int64_t n_features, int64_t ldc,

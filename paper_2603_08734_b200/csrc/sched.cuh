@@ -8,13 +8,16 @@
 
 namespace rsh {
 
-constexpr int kChunk = 32;      // blocks per window work unit
+constexpr int kChunkMin = 32;   // smallest blocks-per-unit a schedule may use (sizes buffers)
+constexpr int kChunkCC = 32;    // CUDA-core path: one warp walks a unit serially
+constexpr int kChunkTC = 256;   // tensor-core path: a unit stays in one TMEM accumulator
 constexpr int kResRows = 8;     // residual rows per unit
 constexpr int kZeroRows = 32;   // uncovered rows per unit
 
 enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
 
 // header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
+//         [5]=blocks per window unit (the fixed chunking)
 // counters: uint32 [0]=next unit [1]=warps done
 struct Sched {
   int64_t* header;
@@ -56,7 +59,7 @@ inline size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_
   s->pc = cv.take<int32_t>(n_blocks + 1);
   s->uncov_flag = cv.take<uint8_t>(n_rows + 1);
   s->uncovered = cv.take<int32_t>(n_rows + 1);
-  s->max_units = E + n_blocks / kChunk + 1 + (n_res + kResRows - 1) / kResRows + (n_rows + kZeroRows - 1) / kZeroRows + 4;
+  s->max_units = E + n_blocks / kChunkMin + 1 + (n_res + kResRows - 1) / kResRows + (n_rows + kZeroRows - 1) / kZeroRows + 4;
   s->units = cv.take<int4>(s->max_units);
   s->unit_cost = cv.take<int64_t>(s->max_units + 1);
   s->unit_cost_raw = cv.take<int64_t>(s->max_units + 1);
@@ -144,6 +147,7 @@ struct SpmmArgs {
   int32_t window_size;
   Sched s;
   void* partials;
+  int32_t flags;  // tensor-core path knobs (bit 1: skip the consumer-side proxy fence)
 };
 
 

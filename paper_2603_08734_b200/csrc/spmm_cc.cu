@@ -8,7 +8,7 @@
 //     memset and then overwritten.
 //   * consecutive entries sharing a row_window_id form one logical window whose block
 //     sequence is independent of how it was split (execute.py:136-152).  Here a logical window
-//     is cut at FIXED block offsets (kChunk blocks) from its first block; chunk partials are
+//     is cut at FIXED block offsets (the schedule's chunk) from its first block; chunk partials are
 //     summed in chunk order by whichever warp finishes last (atomic ticket), so the result is
 //     bit-identical for every max_blocks_per_item and every scheduling order.
 //   * accumulate_precision f32 / f64 (execute.py:33-49): AccT = float / double.
@@ -25,7 +25,8 @@ __global__ void k_group_heads(const int32_t* __restrict__ rwid, int64_t E, uint8
     flag[e] = (e == 0 || rwid[e] != rwid[e - 1]);
 }
 
-__global__ void k_groups(const int32_t* __restrict__ rwid, const int64_t* __restrict__ rwoff, int64_t E, Sched s) {
+__global__ void k_groups(const int32_t* __restrict__ rwid, const int64_t* __restrict__ rwoff, int64_t E, Sched s,
+                         int32_t chunk) {
   int64_t G = s.header[0];
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= E; g += (int64_t)gridDim.x * blockDim.x) {
     int32_t nch = 0, multi = 0;
@@ -35,7 +36,7 @@ __global__ void k_groups(const int32_t* __restrict__ rwid, const int64_t* __rest
       s.grp_rid[g] = rwid[e0];
       s.grp_b0[g] = (int32_t)b0;
       s.grp_b1[g] = (int32_t)b1;
-      int64_t c = (b1 - b0 + kChunk - 1) / kChunk;
+      int64_t c = (b1 - b0 + chunk - 1) / chunk;
       nch = (int32_t)(c > 1 ? c : 1);
       multi = nch > 1 ? nch : 0;
       s.grp_nch[g] = nch;
@@ -46,14 +47,14 @@ __global__ void k_groups(const int32_t* __restrict__ rwid, const int64_t* __rest
   }
 }
 
-__global__ void k_window_units(int64_t E, Sched s) {
+__global__ void k_window_units(int64_t E, Sched s, int32_t chunk) {
   int64_t G = s.header[0];
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
     int32_t nch = s.grp_nch[g], b0 = s.grp_b0[g], b1 = s.grp_b1[g];
     int32_t base = s.unit_base[g];
     s.grp_slot[g] = nch > 1 ? s.slot_base[g] : -1;
     for (int32_t k = 0; k < nch; ++k) {
-      int32_t lo = b0 + k * kChunk, hi = lo + kChunk < b1 ? lo + kChunk : b1;
+      int32_t lo = b0 + k * chunk, hi = lo + chunk < b1 ? lo + chunk : b1;
       s.units[base + k] = make_int4(kUnitWindow | (k << 2), (int32_t)g, lo, hi);
       s.unit_cost_raw[base + k] = (hi - lo) + 1;  // blocks gathered + one window of C rows
     }
@@ -76,7 +77,7 @@ __global__ void k_popc32(const unsigned long long* __restrict__ bm, int64_t nb, 
     pc[i] = i < nb ? __popcll(bm[i]) : 0;
 }
 
-__global__ void k_finish_header(Sched s, int64_t E, int64_t n_res) {
+__global__ void k_finish_header(Sched s, int64_t E, int64_t n_res, int32_t chunk) {
   int64_t uw = s.unit_base[E];
   int64_t ru = (n_res + kResRows - 1) / kResRows;
   int64_t z = s.header[4];
@@ -84,6 +85,7 @@ __global__ void k_finish_header(Sched s, int64_t E, int64_t n_res) {
   s.header[1] = uw;
   s.header[2] = uw + ru + zu;
   s.header[3] = s.slot_base[E];
+  s.header[5] = chunk;
   s.counters[0] = 0;
   s.counters[1] = 0;
 }
@@ -106,6 +108,89 @@ __global__ void k_tail_units(Sched s, int64_t n_res) {
 // ------------------------------------------------------------------------------------------
 // the persistent CUDA-core kernel: one warp per work unit, units fetched dynamically
 // ------------------------------------------------------------------------------------------
+
+// Software-pipelined window chunk: the set bits of a block are consumed in bit order (row i
+// unrolled so the accumulator row stays static), while the B rows of the next kPF nonzeros are
+// already in flight -- across row and block boundaries.  Two metadata cursors run one block
+// ahead: the gather cursor (bitmap + col ids) and the consume cursor (bitmap + packed values).
+// kPF + 1 gathers per warp are outstanding instead of one.
+template <int VEC, class BT, class AccT, int kPF>
+__device__ __forceinline__ void window_chunk_pf(const SpmmArgs& a, int32_t b0, int32_t b1, int f0, bool active,
+                                                AccT (&acc)[8][VEC]) {
+  const int lane = threadIdx.x & 31;
+  const BT* B = reinterpret_cast<const BT*>(a.B);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) acc[i][t] = AccT(0);
+  if (b0 >= b1) return;
+  auto gmeta = [&](int32_t blk, unsigned long long& bm, int32_t& col) {
+    bm = __ldg(a.bitmaps + blk);
+    col = lane < 8 ? __ldg(a.col_id + (int64_t)blk * 8 + lane) : 0;
+  };
+  auto cmeta = [&](int32_t blk, unsigned long long& bm, float& v0, float& v1) {
+    bm = __ldg(a.bitmaps + blk);
+    const int32_t vs = __ldg(a.s.vstart + blk);
+    const int nv = __popcll(bm);
+    v0 = lane < nv ? __ldg(a.tc_values + vs + lane) : 0.f;
+    v1 = lane + 32 < nv ? __ldg(a.tc_values + vs + 32 + lane) : 0.f;
+  };
+  // gather cursor: next nonzero whose B row has not been requested
+  int32_t gblk = b0;
+  unsigned long long grem, gbm_n = 0;
+  int32_t gcol, gcol_n = 0;
+  gmeta(b0, grem, gcol);
+  if (b0 + 1 < b1) gmeta(b0 + 1, gbm_n, gcol_n);
+  auto issue = [&](float (&dst)[VEC]) {
+    while (grem == 0 && gblk + 1 < b1) {
+      ++gblk;
+      grem = gbm_n;
+      gcol = gcol_n;
+      if (gblk + 1 < b1) gmeta(gblk + 1, gbm_n, gcol_n);
+    }
+    if (grem == 0) return;
+    const int bit = __ffsll((long long)grem) - 1;
+    grem &= grem - 1;
+    const int32_t c = __shfl_sync(0xffffffffu, gcol, bit & 7);
+    if (active) load_vec<VEC, BT>(B + (int64_t)c * a.ldb + f0, dst);
+  };
+  float ring[kPF][VEC];
+#pragma unroll
+  for (int p = 0; p < kPF; ++p) issue(ring[p]);
+  // consume cursor
+  unsigned long long cbm;
+  float cv0, cv1;
+  cmeta(b0, cbm, cv0, cv1);
+  for (int32_t blk = b0; blk < b1; ++blk) {
+    const unsigned long long bm = cbm;
+    const float v0 = cv0, v1 = cv1;
+    if (blk + 1 < b1) cmeta(blk + 1, cbm, cv0, cv1);
+    int kk = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t rb = uint32_t(bm >> (8 * i)) & 0xffu;
+      while (rb) {
+        rb &= rb - 1;
+        const float va = __shfl_sync(0xffffffffu, v0, kk & 31);
+        const float vb = __shfl_sync(0xffffffffu, v1, kk & 31);
+        const AccT v = AccT(kk < 32 ? va : vb);
+        ++kk;
+        float bv[VEC];
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) bv[t] = ring[0][t];
+#pragma unroll
+        for (int p = 0; p + 1 < kPF; ++p)
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) ring[p][t] = ring[p + 1][t];
+        issue(ring[kPF - 1]);
+        if (active) {
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) acc[i][t] = fma(v, AccT(bv[t]), acc[i][t]);
+        }
+      }
+    }
+  }
+}
 
 template <int VEC, class BT, class AccT>
 __device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int32_t b1, int f0, bool active,
@@ -148,7 +233,7 @@ __device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int3
 }
 
 template <int VEC, class BT, class AccT>
-__global__ void __launch_bounds__(kThreads) k_spmm_cc(SpmmArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k_spmm_cc(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t total_units = a.s.header[2];
   const int n_fc = (a.N + 32 * VEC - 1) / (32 * VEC);
@@ -169,7 +254,12 @@ __global__ void __launch_bounds__(kThreads) k_spmm_cc(SpmmArgs a) {
         int f0 = fc * 32 * VEC + lane * VEC;
         bool active = f0 < a.N;
         AccT acc[8][VEC];
-        window_chunk<VEC, BT, AccT>(a, un.z, un.w, f0, active, acc);
+        bool pf = false;
+        if constexpr (std::is_same<AccT, float>::value && VEC <= 4) pf = !(a.flags & 1);
+        if (pf)
+          window_chunk_pf<VEC, BT, AccT, 3>(a, un.z, un.w, f0, active, acc);
+        else
+          window_chunk<VEC, BT, AccT>(a, un.z, un.w, f0, active, acc);
         if (slot < 0) {
           if (active) {
 #pragma unroll
@@ -200,11 +290,24 @@ __global__ void __launch_bounds__(kThreads) k_spmm_cc(SpmmArgs a) {
               AccT sum[VEC];
 #pragma unroll
               for (int q = 0; q < VEC; ++q) sum[q] = AccT(0);
-              for (int kk = 0; kk < nch; ++kk) {
-                const AccT* part = reinterpret_cast<const AccT*>(a.partials) + ((int64_t)(slot + kk) * 8 + i) * a.N + f0;
+              // partials summed in chunk order; loads issued 8 chunks ahead of the adds
+              const AccT* part0 = reinterpret_cast<const AccT*>(a.partials) + (int64_t)i * a.N + f0;
+              const int64_t cstride = (int64_t)8 * a.N;
+              int kk = 0;
+              for (; kk + 8 <= nch; kk += 8) {
+                AccT buf[8][VEC];
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) sum[q] += __ldcg(part + q);
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                  for (int q = 0; q < VEC; ++q) buf[u][q] = __ldcg(part0 + (int64_t)(slot + kk + u) * cstride + q);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                  for (int q = 0; q < VEC; ++q) sum[q] += buf[u][q];
               }
+              for (; kk < nch; ++kk)
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) sum[q] += __ldcg(part0 + (int64_t)(slot + kk) * cstride + q);
               store_c<VEC, AccT>(a.C + (rid + i) * a.ldc + f0, sum);
             }
           }
@@ -277,13 +380,17 @@ size_t rsh_schedule_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, i
 }
 
 // Work-unit schedule for one RS-Tile format (execute.py:136-168 restated as device data):
-// logical windows, fixed-offset chunks, partial slots, per-block value starts, uncovered rows.
+// logical windows, fixed-offset chunks of chunk_blocks blocks (kChunkCC for the CUDA-core
+// kernel, kChunkTC for the tensor-core kernel), partial slots, per-block value starts,
+// uncovered rows.
 // header_out (device int64[8]) receives [groups, window units, units, partial slots, uncovered].
 int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_id, const int64_t* row_window_offset,
                  int64_t n_entries, const uint64_t* bitmaps, int64_t n_blocks, const int32_t* res_row_id, int64_t n_res,
-                 void* sched, size_t sched_bytes, int64_t* header_out, cudaStream_t st) {
+                 int32_t chunk_blocks, void* sched, size_t sched_bytes, int64_t* header_out, cudaStream_t st) {
   if (n_rows < 0 || n_entries < 0 || n_blocks < 0 || n_res < 0 || window_size < 1 || window_size > 8)
     return fail(kInvalid, "rsh_schedule: bad sizes");
+  if (chunk_blocks < kChunkMin || chunk_blocks > (1 << 20))
+    return fail(kInvalid, "rsh_schedule: chunk_blocks %d outside [%d, 2^20]", chunk_blocks, kChunkMin);
   if (n_blocks >= (1LL << 31) || n_rows >= (1LL << 31)) return fail(kInvalid, "rsh_schedule: index limit");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
@@ -298,7 +405,7 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
     RSH_CUDA(cub::DeviceSelect::Flagged(s.cub, cb, cub::CountingInputIterator<int32_t>(0), s.flags, s.head,
                                         s.header, (int)E, st));
   }
-  k_groups<<<grid_1d(E + 1), kThreads, 0, st>>>(row_window_id, row_window_offset, E, s);
+  k_groups<<<grid_1d(E + 1), kThreads, 0, st>>>(row_window_id, row_window_offset, E, s, chunk_blocks);
   RSH_LAUNCHED("k_groups");
   // unit_base currently holds nch; scan it (through grp_slot as scratch), multi -> slot_base
   cb = s.cub_bytes;
@@ -308,7 +415,7 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.grp_multi, s.slot_base, (int)(E + 1), st));
   RSH_CUDA(cudaMemsetAsync(s.unit_cost_raw, 0, (s.max_units + 1) * sizeof(int64_t), st));
   if (E) {
-    k_window_units<<<grid_1d(E), kThreads, 0, st>>>(E, s);
+    k_window_units<<<grid_1d(E), kThreads, 0, st>>>(E, s, chunk_blocks);
     RSH_LAUNCHED("k_window_units");
   }
   cb = s.cub_bytes;
@@ -326,7 +433,7 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
     RSH_CUDA(cub::DeviceSelect::Flagged(s.cub, cb, cub::CountingInputIterator<int32_t>(0), s.uncov_flag, s.uncovered,
                                         s.header + 4, (int)n_rows, st));
   }
-  k_finish_header<<<1, 1, 0, st>>>(s, E, n_res);
+  k_finish_header<<<1, 1, 0, st>>>(s, E, n_res, chunk_blocks);
   k_tail_units<<<grid_1d(n_res / kResRows + n_rows / kZeroRows + 2), kThreads, 0, st>>>(s, n_res);
   RSH_LAUNCHED("schedule tail");
   if (header_out) RSH_CUDA(cudaMemcpyAsync(header_out, s.header, 8 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
@@ -346,7 +453,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 1) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 3) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -367,6 +474,8 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.window_size = window_size;
   a.s = s;
   a.partials = partials;
+  a.flags = accum >> 1;  // bit 0: plain (non-prefetching) window walk
+  accum &= 1;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;
   int vec = 8;

@@ -11,7 +11,7 @@
 //
 // Warp roles per CTA (one CTA per SM, persistent, cost-balanced contiguous unit ranges):
 //   warps 0-3   epilogue: tcgen05.ld -> registers -> streaming C stores (or chunk partials +
-//               ordered ticket reduction for windows longer than kChunk blocks)
+//               ordered ticket reduction for windows longer than one unit)
 //   warps 4-7   MMA issuers, one per pipeline / SM sub-partition (+ TMEM allocation)
 //   warps 8-19  producers, 3 per pipeline: block metadata, gather, decode, mbarrier signalling;
 //               afterwards they take the residual / zero-row units (CUDA-core path) from a
@@ -58,6 +58,29 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   for (uint32_t n = 0; !mbar_try(bar, parity); ++n)
     if (n == (1u << 26)) __trap();
+}
+
+// Optional per-CTA role timing (flags bit 4): cycle counters, read back with rsh_tc_profile().
+constexpr int kProfSlots = 16;
+__device__ unsigned long long g_tc_prof[1024][kProfSlots];
+
+struct Prof {
+  bool on;
+  unsigned long long v[kProfSlots];
+  __device__ void flush(int cta, int lo, int hi) {
+    if (!on) return;
+    for (int i = lo; i < hi; ++i)
+      if (v[i]) atomicAdd(&g_tc_prof[cta & 1023][i], v[i]);
+  }
+};
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, Prof& p, int slot) {
+  if (!p.on) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const long long t = clock64();
+  mbar_wait(bar, parity);
+  p.v[slot] += clock64() - t;
 }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -197,13 +220,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
   const int64_t G = gridDim.x;
   const int64_t u0 = cost_bound(a.s.unit_cost, nwu, (total * (int64_t)blockIdx.x) / G);
   const int64_t u1 = blockIdx.x + 1 == G ? nwu : cost_bound(a.s.unit_cost, nwu, (total * ((int64_t)blockIdx.x + 1)) / G);
+  Prof prof;
+  prof.on = (a.flags & 16) != 0;
+#pragma unroll
+  for (int i = 0; i < kProfSlots; ++i) prof.v[i] = 0;
+  const long long t_begin = clock64();
 
   if (warp >= kProd0) {
     // ---------------------------------------------------------------- producers
     // Pipeline w (of kPipes) owns the units ua = w (mod kPipes) of this CTA, in order, and its own
     // ring of SP stages; its kProdPerPipe producer warps split the pipeline's block sequence
     // m = 0, 1, 2, ... round robin.  Unit metadata (bitmap, value start, 8 col ids of each of
-    // its <= kChunk blocks; lane l <-> block l) is fetched one unit ahead in one coalesced load;
+    // its blocks, 32 at a time; lane l <-> block l) is fetched in coalesced loads;
     // block values are prefetched two blocks ahead into registers.  Per block the warp then only
     // waits for a free stage, issues the 8 row gathers (cp.async, 16 B per lane per row,
     // zero-filled for padding slots) whose completion the hardware reports on the stage's full
@@ -221,16 +249,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
       int4 c0, c1;
       int32_t z, nb;
     };
-    auto load_meta = [&](int64_t u, Meta& M) {
+    // batches: up to 32 consecutive blocks of one unit of this pipeline
+    auto load_meta = [&](int64_t u, int off, Meta& M) {
       const int4 un = a.s.units[u];
-      M.z = un.z;
-      M.nb = un.w - un.z;
-      const int64_t blk = (int64_t)un.z + lane;
+      M.z = un.z + off;
+      M.nb = min(32, un.w - M.z);
+      const int64_t blk = (int64_t)M.z + lane;
       const bool mine = lane < M.nb;
       M.bm = mine ? __ldg(a.bitmaps + blk) : 0ull;
       M.vs = mine ? __ldg(a.s.vstart + blk) : 0;
       M.c0 = mine ? __ldg(reinterpret_cast<const int4*>(a.col_id + blk * 8)) : make_int4(0, 0, 0, 0);
       M.c1 = mine ? __ldg(reinterpret_cast<const int4*>(a.col_id + blk * 8) + 1) : make_int4(0, 0, 0, 0);
+    };
+    auto skip_empty = [&](int64_t& u) {
+      while (u < u1) {
+        const int4 un = a.s.units[u];
+        if (un.z != un.w) break;
+        u += kPipes;
+      }
+    };
+    auto step = [&](int64_t& u, int& off) {
+      off += 32;
+      if (u < u1) {
+        const int4 un = a.s.units[u];
+        if (un.z + off < un.w) return;
+      }
+      u += kPipes;
+      off = 0;
+      skip_empty(u);
     };
     auto load_vals = [&](const Meta& M, int l, float& v0, float& v1) {
       const unsigned long long bm = __shfl_sync(0xffffffffu, M.bm, l);
@@ -241,10 +287,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
     };
     Meta cur, nxt;
     int64_t u = u0 + w;
-    if (u < u1) load_meta(u, cur);
-    int64_t m0 = 0;  // pipeline block count before the current unit
-    for (; u < u1; u += kPipes) {
-      if (u + kPipes < u1) load_meta(u + kPipes, nxt);
+    int off = 0;
+    skip_empty(u);
+    if (u < u1) load_meta(u, off, cur);
+    int64_t m0 = 0;  // pipeline block count before the current batch
+    while (u < u1) {
+      int64_t un_ = u;
+      int off_ = off;
+      step(un_, off_);
+      if (un_ < u1) load_meta(un_, off_, nxt);
       const int nb = cur.nb;
       const int first = (int)(((q - m0) % kProdPerPipe + kProdPerPipe) % kProdPerPipe);
       float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f;  // values of the next two blocks
@@ -271,7 +322,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
         x |= x >> 16;
         x |= x >> 8;
         const uint32_t cm = (uint32_t)x & 0xffu;
-        mbar_wait(empty + s, (uint32_t)(((m / SP) & 1) ^ 1));
+        mbar_wait_t(empty + s, (uint32_t)(((m / SP) & 1) ^ 1), prof, 0);
         const uint32_t stageA = smem_u32(sA + (size_t)s * MT * kTileBytes);
         constexpr int kChunksPerTileRow = 8 * EB;  // 16-B chunks of 128 features
         constexpr int kChunksPerRow = MT * kChunksPerTileRow;
@@ -284,7 +335,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
             const int t = cc / kChunksPerTileRow;
             const int byte = (cc % kChunksPerTileRow) * 16;
             const uint32_t dst = stageA + t * kTileBytes + a_offset<EB>(byte >> 7, k, (byte & 127) >> 4);
-            cp16<kL1>(dst, src_row + cc * 16, nbytes);
+            if (!(a.flags & 4)) cp16<kL1>(dst, src_row + cc * 16, nbytes);  // bit 2: perf probe, no gathers
           }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
@@ -313,8 +364,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
       }
       m0 += nb;
       cur = nxt;
+      u = un_;
+      off = off_;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    const long long t_prod = clock64();
+    prof.v[1] = t_prod - t_begin;
 
     // residual and zero-row units (CUDA-core), fetched dynamically across the grid
     const int64_t nunits = a.s.header[2];
@@ -329,6 +384,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
       if ((un.x & 3) == kUnitResidual) residual_rows<kVec, BT, float>(a, un.y, un.z, n_fc);
       else zero_rows<kVec>(a, un.y, un.z);
     }
+    prof.v[2] = clock64() - t_prod;
+    if (lane == 0) prof.flush(blockIdx.x, 0, 3);
     __syncwarp();
     if (lane == 0) {
       uint32_t producers = gridDim.x * kProdWarps;
@@ -352,7 +409,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
       for (int64_t u = u0 + w; u < u1; u += kPipes, ua += kPipes) {
         const int4 un = a.s.units[u];
         const int slot = (int)(ua % NACC);
-        mbar_wait(tempty + slot, (uint32_t)(((ua / NACC) & 1) ^ 1));
+        mbar_wait_t(tempty + slot, (uint32_t)(((ua / NACC) & 1) ^ 1), prof, 4);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (un.z == un.w) {
           mbar_arrive(tfull + slot);
@@ -360,10 +417,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
         }
         for (int32_t blk = un.z; blk < un.w; ++blk, ++m) {
           const int s = w * SP + (int)(m % SP);
-          mbar_wait(full + s, (uint32_t)((m / SP) & 1));
+          mbar_wait_t(full + s, (uint32_t)((m / SP) & 1), prof, 3);
           // the gathered rows were written by cp.async (generic proxy) and observed through
           // the barrier; make them visible to the tensor core's async-proxy operand reads
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (!(a.flags & 2)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t bdesc = umma_desc(smem_u32(sB + (size_t)s * kBopBytes), 128, 256, 0);
 #pragma unroll
@@ -371,12 +428,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
             const uint64_t adesc =
                 umma_desc(smem_u32(sA + ((size_t)s * MT + t) * kTileBytes), Kind<BT>::lbo, Kind<BT>::sbo,
                           Kind<BT>::layout);
-            mma<BT>(tmem + (uint32_t)((slot * MT + t) * 8), adesc, bdesc, idesc, blk > un.z ? 1u : 0u);
+            if (!(a.flags & 8))  // bit 3: perf probe, no MMA
+              mma<BT>(tmem + (uint32_t)((slot * MT + t) * 8), adesc, bdesc, idesc, blk > un.z ? 1u : 0u);
           }
           umma_commit(empty + s);
         }
         umma_commit(tfull + slot);
       }
+      prof.v[5] = clock64() - t_begin;
+      prof.flush(blockIdx.x, 3, 6);
     }
     __syncwarp();
   } else {
@@ -386,7 +446,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
     for (int64_t u = u0; u < u1; ++u, ++ua) {
       int4 un = a.s.units[u];
       const int slot = (int)(ua % NACC);
-      mbar_wait(tfull + slot, (uint32_t)((ua / NACC) & 1));
+      mbar_wait_t(tfull + slot, (uint32_t)((ua / NACC) & 1), prof, 6);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int32_t g = un.y, k = un.x >> 2;
       const int64_t rid = a.s.grp_rid[g];
@@ -428,30 +488,52 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
         for (int t = 0; t < MT; ++t)
 #pragma unroll
           for (int i = 0; i < 8; ++i) __stcg(part + (int64_t)i * a.N + t * 128 + f_in_tile, r[t][i]);
-        __threadfence();
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-        if (threadIdx.x == 0) misc[1] = atomicAdd(a.s.ticket + g, 1u);
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        // one thread publishes for the whole epilogue group (bar.sync orders the others' stores
+        // before its fence) and, if it took the last ticket, acquires for everyone
+        const long long tp = prof.on ? clock64() : 0;
         const int32_t nch = a.s.grp_nch[g];
-        if ((int32_t)misc[1] == nch - 1) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (threadIdx.x == 0) {
           __threadfence();
+          const uint32_t t = atomicAdd(a.s.ticket + g, 1u);
+          if ((int32_t)t == nch - 1) __threadfence();
+          misc[1] = t;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if ((int32_t)misc[1] == nch - 1) {
 #pragma unroll
           for (int t = 0; t < MT; ++t) {
             const int64_t f = t * 128 + f_in_tile;
             for (int i = 0; i < avail; ++i) {
+              // partials summed in chunk order; loads issued 8 chunks ahead of the adds
+              const float* part0 = reinterpret_cast<const float*>(a.partials) + (int64_t)i * a.N + f;
+              const int64_t cstride = (int64_t)8 * a.N;
               float sum = 0.f;
-              for (int kk = 0; kk < nch; ++kk)
-                sum += __ldcg(reinterpret_cast<const float*>(a.partials) + ((int64_t)(pslot + kk) * 8 + i) * a.N + f);
+              int kk = 0;
+              for (; kk + 8 <= nch; kk += 8) {
+                float buf[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) buf[u] = __ldcg(part0 + (int64_t)(pslot + kk + u) * cstride);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) sum += buf[u];
+              }
+              for (; kk < nch; ++kk) sum += __ldcg(part0 + (int64_t)(pslot + kk) * cstride);
               __stcs(a.C + (rid + i) * a.ldc + f, sum);
             }
           }
           if (threadIdx.x == 0) a.s.ticket[g] = 0;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (prof.on) prof.v[8] += clock64() - tp;
       }
     }
   }
 
+  if (warp == 0 && lane == 0) {
+    prof.v[7] = clock64() - t_begin;
+    prof.flush(blockIdx.x, 6, 9);
+  }
+  if (threadIdx.x == 0 && prof.on) atomicAdd(&g_tc_prof[blockIdx.x & 1023][9], (unsigned long long)(clock64() - t_begin));
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == kMmaWarp0) {
@@ -487,6 +569,14 @@ using namespace rsh;
 
 extern "C" {
 
+// Debug: copy the per-CTA role cycle counters (flags bit 4) to host_out[1024 * 16] and clear them.
+int rsh_tc_profile(unsigned long long* host_out) {
+  RSH_CUDA(cudaMemcpyFromSymbol(host_out, tc::g_tc_prof, sizeof(tc::g_tc_prof)));
+  static unsigned long long zeros[1024][tc::kProfSlots];
+  RSH_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof, zeros, sizeof(zeros)));
+  return kOk;
+}
+
 // Tensor-core hybrid SpMM (execute.py:155-218 semantics, TF32 / BF16 / FP16 operands, fp32
 // accumulation).  Requirements: N in {128, 256}, f32 accumulation, 16-byte aligned B rows.
 // l1: 1 = gather through L1 (cp.async.ca), 0 = L2 only (cp.async.cg).
@@ -520,6 +610,8 @@ int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.window_size = window_size;
   a.s = s;
   a.partials = partials;
+  a.flags = l1;
+  l1 &= 1;
   const int mt = (int)(N / 128);
   if (b_dtype == 0) {
     if (mt == 1) return l1 ? tc::launch<float, 1, 48, true>(a, st) : tc::launch<float, 1, 48, false>(a, st);

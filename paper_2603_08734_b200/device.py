@@ -97,7 +97,7 @@ class DeviceTile:
     res_offset: torch.Tensor         # int64 [R+1]
     res_col_id: torch.Tensor         # int32 [res nnz]
     res_values: torch.Tensor         # float32 [res nnz]
-    _plan: "SpmmPlan | None" = field(default=None, repr=False)
+    _plan: "dict | SpmmPlan | None" = field(default=None, repr=False)
 
     @property
     def n_entries(self) -> int:
@@ -275,16 +275,21 @@ def build_device(a: DeviceCsr, window_size=8, tau_nnz=None, tau_inc=None, max_bl
 _BDT = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 
 
-class SpmmPlan:
-    """Persistent-kernel work schedule of one DeviceTile (built once, reused every call)."""
+CHUNK_CC = 32    # blocks per work unit for the CUDA-core kernel (csrc/sched.cuh kChunkCC)
+CHUNK_TC = 256   # ... and for the tensor-core kernel (kChunkTC)
 
-    def __init__(self, t: DeviceTile, stream=None):
+
+class SpmmPlan:
+    """Persistent-kernel work schedule of one DeviceTile for one unit size (built once, reused)."""
+
+    def __init__(self, t: DeviceTile, chunk: int = CHUNK_CC, stream=None):
         dev = t.device
+        self.chunk = chunk
         self.nbytes = lib().rsh_schedule_bytes(t.n_rows, t.n_entries, t.n_blocks, t.n_res)
         self.buf = _ws(self.nbytes, dev)
         hdr = torch.zeros(8, dtype=torch.int64, device=dev)
         call("rsh_schedule", t.n_rows, t.window_size, _ptr(t.row_window_id), _ptr(t.row_window_offset),
-             t.n_entries, _ptr(t.bitmaps), t.n_blocks, _ptr(t.res_row_id), t.n_res, _ptr(self.buf),
+             t.n_entries, _ptr(t.bitmaps), t.n_blocks, _ptr(t.res_row_id), t.n_res, chunk, _ptr(self.buf),
              self.nbytes, _ptr(hdr), _stream(stream))
         h = hdr.cpu().tolist()
         self.groups, self.window_units, self.units, self.partial_slots, self.uncovered = h[:5]
@@ -298,10 +303,15 @@ class SpmmPlan:
         return self._partials[key]
 
 
-def spmm_plan(t: DeviceTile) -> SpmmPlan:
+def spmm_plan(t: DeviceTile, chunk: int = CHUNK_CC) -> SpmmPlan:
+    """The cached schedule of ``t`` for units of ``chunk`` blocks."""
     if t._plan is None:
-        t._plan = SpmmPlan(t)
-    return t._plan
+        t._plan = {}
+    elif isinstance(t._plan, SpmmPlan):  # a single prebuilt schedule handed over by a caller
+        t._plan = {t._plan.chunk: t._plan}
+    if chunk not in t._plan:
+        t._plan[chunk] = SpmmPlan(t, chunk)
+    return t._plan[chunk]
 
 
 def tc_eligible(t: DeviceTile, b: torch.Tensor, accumulate: str = "f32") -> bool:
@@ -327,7 +337,7 @@ def resolve_math(math: str, b: torch.Tensor, t: DeviceTile, accumulate: str) -> 
 
 
 def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None, accumulate: str = "f32",
-                stream=None, math: str = "auto", l1: bool = True) -> torch.Tensor:
+                stream=None, math: str = "auto", l1: bool = True, cc_flags: int = 0) -> torch.Tensor:
     """C = A @ B with A an RS-Tile on device; B [n_cols, N] f32/bf16/f16 row-major on device.
     Returns (or fills) C [n_rows, N] float32.  accumulate: "f32" | "f64" (execute.py:33-49);
     math: "auto" | "fp32" (CUDA-core FMA) | "tf32" (tensor cores, see resolve_math)."""
@@ -347,13 +357,13 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
     if t.n_rows == 0 or N == 0:
         return out
     acc = {"f32": 0, "f64": 1}[accumulate]
-    plan = spmm_plan(t)
-    part = plan.partials(N, acc, b.device)
     path = resolve_math(math, b, t, accumulate)
+    plan = spmm_plan(t, CHUNK_TC if path == "tc" else CHUNK_CC)
+    part = plan.partials(N, acc, b.device)
     call("rsh_spmm_tc" if path == "tc" else "rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
          _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),
          _ptr(t.res_values), t.n_res, _ptr(b), b.stride(0), _BDT[b.dtype], N, _ptr(out), out.stride(0),
-         int(l1) if path == "tc" else acc, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
+         int(l1) if path == "tc" else acc | (cc_flags << 1), _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
     return out
 
 

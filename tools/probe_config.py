@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--math", default="auto")
     ap.add_argument("--l1", type=int, default=1)
+    ap.add_argument("--ccflags", type=int, default=0)
     args = ap.parse_args()
     t0 = time.time()
     a = synth.workload_matrix(args.workload)
@@ -45,20 +46,22 @@ def main():
           f"ws={t.window_size} tile bytes={t.nbytes() / 1e6:.1f} MB", flush=True)
     t1 = time.time()
     plan = spmm_plan(t)
+    from paper_2603_08734_b200.device import CHUNK_TC
+    spmm_plan(t, CHUNK_TC)
     torch.cuda.synchronize()
     print(f"schedule {1e3 * (time.time() - t1):.1f} ms: groups={plan.groups} units={plan.units} "
           f"slots={plan.partial_slots} uncovered={plan.uncovered}", flush=True)
     out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(3):
-        spmm_device(t, bt, out=out, math=args.math, l1=bool(args.l1))
+        spmm_device(t, bt, out=out, math=args.math, l1=args.l1, cc_flags=args.ccflags)
     torch.cuda.synchronize()
     times = []
     for _ in range(args.iters):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        spmm_device(t, bt, out=out, math=args.math, l1=bool(args.l1))
+        spmm_device(t, bt, out=out, math=args.math, l1=args.l1, cc_flags=args.ccflags)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))

@@ -109,89 +109,6 @@ __global__ void k_tail_units(Sched s, int64_t n_res) {
 // the persistent CUDA-core kernel: one warp per work unit, units fetched dynamically
 // ------------------------------------------------------------------------------------------
 
-// Software-pipelined window chunk: the set bits of a block are consumed in bit order (row i
-// unrolled so the accumulator row stays static), while the B rows of the next kPF nonzeros are
-// already in flight -- across row and block boundaries.  Two metadata cursors run one block
-// ahead: the gather cursor (bitmap + col ids) and the consume cursor (bitmap + packed values).
-// kPF + 1 gathers per warp are outstanding instead of one.
-template <int VEC, class BT, class AccT, int kPF>
-__device__ __forceinline__ void window_chunk_pf(const SpmmArgs& a, int32_t b0, int32_t b1, int f0, bool active,
-                                                AccT (&acc)[8][VEC]) {
-  const int lane = threadIdx.x & 31;
-  const BT* B = reinterpret_cast<const BT*>(a.B);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int t = 0; t < VEC; ++t) acc[i][t] = AccT(0);
-  if (b0 >= b1) return;
-  auto gmeta = [&](int32_t blk, unsigned long long& bm, int32_t& col) {
-    bm = __ldg(a.bitmaps + blk);
-    col = lane < 8 ? __ldg(a.col_id + (int64_t)blk * 8 + lane) : 0;
-  };
-  auto cmeta = [&](int32_t blk, unsigned long long& bm, float& v0, float& v1) {
-    bm = __ldg(a.bitmaps + blk);
-    const int32_t vs = __ldg(a.s.vstart + blk);
-    const int nv = __popcll(bm);
-    v0 = lane < nv ? __ldg(a.tc_values + vs + lane) : 0.f;
-    v1 = lane + 32 < nv ? __ldg(a.tc_values + vs + 32 + lane) : 0.f;
-  };
-  // gather cursor: next nonzero whose B row has not been requested
-  int32_t gblk = b0;
-  unsigned long long grem, gbm_n = 0;
-  int32_t gcol, gcol_n = 0;
-  gmeta(b0, grem, gcol);
-  if (b0 + 1 < b1) gmeta(b0 + 1, gbm_n, gcol_n);
-  auto issue = [&](float (&dst)[VEC]) {
-    while (grem == 0 && gblk + 1 < b1) {
-      ++gblk;
-      grem = gbm_n;
-      gcol = gcol_n;
-      if (gblk + 1 < b1) gmeta(gblk + 1, gbm_n, gcol_n);
-    }
-    if (grem == 0) return;
-    const int bit = __ffsll((long long)grem) - 1;
-    grem &= grem - 1;
-    const int32_t c = __shfl_sync(0xffffffffu, gcol, bit & 7);
-    if (active) load_vec<VEC, BT>(B + (int64_t)c * a.ldb + f0, dst);
-  };
-  float ring[kPF][VEC];
-#pragma unroll
-  for (int p = 0; p < kPF; ++p) issue(ring[p]);
-  // consume cursor
-  unsigned long long cbm;
-  float cv0, cv1;
-  cmeta(b0, cbm, cv0, cv1);
-  for (int32_t blk = b0; blk < b1; ++blk) {
-    const unsigned long long bm = cbm;
-    const float v0 = cv0, v1 = cv1;
-    if (blk + 1 < b1) cmeta(blk + 1, cbm, cv0, cv1);
-    int kk = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      uint32_t rb = uint32_t(bm >> (8 * i)) & 0xffu;
-      while (rb) {
-        rb &= rb - 1;
-        const float va = __shfl_sync(0xffffffffu, v0, kk & 31);
-        const float vb = __shfl_sync(0xffffffffu, v1, kk & 31);
-        const AccT v = AccT(kk < 32 ? va : vb);
-        ++kk;
-        float bv[VEC];
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) bv[t] = ring[0][t];
-#pragma unroll
-        for (int p = 0; p + 1 < kPF; ++p)
-#pragma unroll
-          for (int t = 0; t < VEC; ++t) ring[p][t] = ring[p + 1][t];
-        issue(ring[kPF - 1]);
-        if (active) {
-#pragma unroll
-          for (int t = 0; t < VEC; ++t) acc[i][t] = fma(v, AccT(bv[t]), acc[i][t]);
-        }
-      }
-    }
-  }
-}
-
 template <int VEC, class BT, class AccT>
 __device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int32_t b1, int f0, bool active,
                                              AccT (&acc)[8][VEC]) {
@@ -233,7 +150,7 @@ __device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int3
 }
 
 template <int VEC, class BT, class AccT>
-__global__ void __launch_bounds__(kThreads, 3) k_spmm_cc(SpmmArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_spmm_cc(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t total_units = a.s.header[2];
   const int n_fc = (a.N + 32 * VEC - 1) / (32 * VEC);
@@ -254,12 +171,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_cc(SpmmArgs a) {
         int f0 = fc * 32 * VEC + lane * VEC;
         bool active = f0 < a.N;
         AccT acc[8][VEC];
-        bool pf = false;
-        if constexpr (std::is_same<AccT, float>::value && VEC <= 4) pf = !(a.flags & 1);
-        if (pf)
-          window_chunk_pf<VEC, BT, AccT, 3>(a, un.z, un.w, f0, active, acc);
-        else
-          window_chunk<VEC, BT, AccT>(a, un.z, un.w, f0, active, acc);
+        window_chunk<VEC, BT, AccT>(a, un.z, un.w, f0, active, acc);
         if (slot < 0) {
           if (active) {
 #pragma unroll
@@ -453,7 +365,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 3) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 1) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -474,8 +386,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.window_size = window_size;
   a.s = s;
   a.partials = partials;
-  a.flags = accum >> 1;  // bit 0: plain (non-prefetching) window walk
-  accum &= 1;
+  a.flags = 0;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;
   int vec = 8;

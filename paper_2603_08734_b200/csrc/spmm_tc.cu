@@ -13,7 +13,8 @@
 //   warps 0-3   epilogue: tcgen05.ld -> registers -> streaming C stores (or chunk partials +
 //               ordered ticket reduction for windows longer than one unit)
 //   warps 4-7   MMA issuers, one per pipeline / SM sub-partition (+ TMEM allocation)
-//   warps 8-19  producers, 3 per pipeline: block metadata, gather, decode, mbarrier signalling;
+//   warps 8-15  producers, 2 per pipeline: block metadata, LDG gather into registers, swizzled
+//               STS into the stage, decode, mbarrier signalling;
 //               afterwards they take the residual / zero-row units (CUDA-core path) from a
 //               global counter.
 // Units ua = w (mod 4) of the CTA's range form pipeline w with its own stage ring, consumed
@@ -24,7 +25,7 @@ namespace rsh {
 namespace tc {
 
 constexpr int kPipes = 4;        // independent producer -> MMA pipelines per CTA
-constexpr int kProdPerPipe = 3;  // producer warps per pipeline
+constexpr int kProdPerPipe = 2;  // producer warps per pipeline
 constexpr int kEpiWarps = 4;
 constexpr int kMmaWarp0 = 4;
 constexpr int kMmaWarps = kPipes;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 33);  // 32 lanes' cp.async completions (noinc) + the decode arrive
+      mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
     for (int s = 0; s < NACC; ++s) {
@@ -285,89 +286,143 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
       v0 = lane < nv ? __ldg(a.tc_values + vs + lane) : 0.f;
       v1 = lane + 32 < nv ? __ldg(a.tc_values + vs + 32 + lane) : 0.f;
     };
+    // ---- block iterator over this producer's share of the pipeline's blocks ----------------
+    struct Blk {
+      int64_t m;
+      unsigned long long bm;
+      int32_t col[8];
+      float v0, v1;
+    };
     Meta cur, nxt;
     int64_t u = u0 + w;
     int off = 0;
     skip_empty(u);
     if (u < u1) load_meta(u, off, cur);
-    int64_t m0 = 0;  // pipeline block count before the current batch
-    while (u < u1) {
+    int64_t m0 = 0;   // pipeline block count before the current batch
+    int l = -1;       // position in the current batch (-1: batch not entered yet)
+    bool have_nxt = false;
+    float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f;  // values of this producer's next two blocks
+    auto enter_batch = [&]() {
       int64_t un_ = u;
       int off_ = off;
       step(un_, off_);
-      if (un_ < u1) load_meta(un_, off_, nxt);
-      const int nb = cur.nb;
-      const int first = (int)(((q - m0) % kProdPerPipe + kProdPerPipe) % kProdPerPipe);
-      float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f;  // values of the next two blocks
-      if (first < nb) load_vals(cur, first, pa0, pa1);
-      if (first + kProdPerPipe < nb) load_vals(cur, first + kProdPerPipe, pb0, pb1);
-      for (int l = first; l < nb; l += kProdPerPipe) {
-        const float v0 = pa0, v1 = pa1;
-        pa0 = pb0;
-        pa1 = pb1;
-        if (l + 2 * kProdPerPipe < nb) load_vals(cur, l + 2 * kProdPerPipe, pb0, pb1);
-        const int64_t m = m0 + l;
-        const int s = w * SP + (int)(m % SP);
-        const unsigned long long bm = __shfl_sync(0xffffffffu, cur.bm, l);
-        int32_t col[8];
-        col[0] = __shfl_sync(0xffffffffu, cur.c0.x, l);
-        col[1] = __shfl_sync(0xffffffffu, cur.c0.y, l);
-        col[2] = __shfl_sync(0xffffffffu, cur.c0.z, l);
-        col[3] = __shfl_sync(0xffffffffu, cur.c0.w, l);
-        col[4] = __shfl_sync(0xffffffffu, cur.c1.x, l);
-        col[5] = __shfl_sync(0xffffffffu, cur.c1.y, l);
-        col[6] = __shfl_sync(0xffffffffu, cur.c1.z, l);
-        col[7] = __shfl_sync(0xffffffffu, cur.c1.w, l);
-        unsigned long long x = bm | (bm >> 32);
-        x |= x >> 16;
-        x |= x >> 8;
-        const uint32_t cm = (uint32_t)x & 0xffu;
-        mbar_wait_t(empty + s, (uint32_t)(((m / SP) & 1) ^ 1), prof, 0);
-        const uint32_t stageA = smem_u32(sA + (size_t)s * MT * kTileBytes);
-        constexpr int kChunksPerTileRow = 8 * EB;  // 16-B chunks of 128 features
-        constexpr int kChunksPerRow = MT * kChunksPerTileRow;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t nbytes = ((cm >> k) & 1u) ? 16u : 0u;
-          const char* src_row = Bbytes + (int64_t)col[k] * row_bytes;
-#pragma unroll
-          for (int cc = lane; cc < kChunksPerRow; cc += 32) {
-            const int t = cc / kChunksPerTileRow;
-            const int byte = (cc % kChunksPerTileRow) * 16;
-            const uint32_t dst = stageA + t * kTileBytes + a_offset<EB>(byte >> 7, k, (byte & 127) >> 4);
-            if (!(a.flags & 4)) cp16<kL1>(dst, src_row + cc * 16, nbytes);  // bit 2: perf probe, no gathers
-          }
-        }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
-        // decode: bit pos = local_row * 8 + local_col, value rank = popc(bits below pos)
-        uint8_t* bop = sB + (size_t)s * kBopBytes;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int pos = lane + 32 * h;
-          const bool set = (bm >> pos) & 1ull;
-          const int rank = pos ? __popcll(bm & ((1ull << pos) - 1ull)) : 0;
-          const float va = __shfl_sync(0xffffffffu, v0, rank & 31);
-          const float vb = __shfl_sync(0xffffffffu, v1, rank & 31);
-          const float v = set ? (rank < 32 ? va : vb) : 0.f;
-          const int i = pos >> 3, k = pos & 7;
-          if constexpr (EB == 4) {
-            *(uint32_t*)(bop + (k >> 2) * 128 + i * 16 + (k & 3) * 4) = to_tf32(v);
-          } else if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
-            *(__nv_bfloat16*)(bop + i * 16 + k * 2) = __float2bfloat16_rn(v);
-          } else {
-            *(__half*)(bop + i * 16 + k * 2) = __float2half_rn(v);
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(full + s);
+      have_nxt = un_ < u1;
+      if (have_nxt) load_meta(un_, off_, nxt);
+      l = (int)(((q - m0) % kProdPerPipe + kProdPerPipe) % kProdPerPipe);
+      if (l < cur.nb) load_vals(cur, l, pa0, pa1);
+      if (l + kProdPerPipe < cur.nb) load_vals(cur, l + kProdPerPipe, pb0, pb1);
+    };
+    auto next = [&](Blk& b) -> bool {
+      for (;;) {
+        if (u >= u1) return false;
+        if (l < 0) enter_batch();
+        if (l < cur.nb) break;
+        // batch exhausted: move to the next one
+        int64_t un_ = u;
+        int off_ = off;
+        step(un_, off_);
+        m0 += cur.nb;
+        cur = nxt;
+        u = un_;
+        off = off_;
+        l = -1;
       }
-      m0 += nb;
-      cur = nxt;
-      u = un_;
-      off = off_;
+      b.m = m0 + l;
+      b.bm = __shfl_sync(0xffffffffu, cur.bm, l);
+      b.col[0] = __shfl_sync(0xffffffffu, cur.c0.x, l);
+      b.col[1] = __shfl_sync(0xffffffffu, cur.c0.y, l);
+      b.col[2] = __shfl_sync(0xffffffffu, cur.c0.z, l);
+      b.col[3] = __shfl_sync(0xffffffffu, cur.c0.w, l);
+      b.col[4] = __shfl_sync(0xffffffffu, cur.c1.x, l);
+      b.col[5] = __shfl_sync(0xffffffffu, cur.c1.y, l);
+      b.col[6] = __shfl_sync(0xffffffffu, cur.c1.z, l);
+      b.col[7] = __shfl_sync(0xffffffffu, cur.c1.w, l);
+      b.v0 = pa0;
+      b.v1 = pa1;
+      pa0 = pb0;
+      pa1 = pb1;
+      if (l + 2 * kProdPerPipe < cur.nb) load_vals(cur, l + 2 * kProdPerPipe, pb0, pb1);
+      l += kProdPerPipe;
+      return true;
+    };
+    // ---- gather (LDG.128 into registers) and store (swizzled STS.128 + decode) -------------
+    constexpr int kChunksPerTileRow = 8 * EB;             // 16-B chunks of 128 features
+    constexpr int kCR = MT * kChunksPerTileRow;           // 16-B chunks per gathered row
+    constexpr int kNC = 8 * kCR / 32;                     // chunks per lane per block
+    static_assert(kNC >= 1 && (8 * kCR) % 32 == 0, "whole warp moves each block");
+    auto issue = [&](const Blk& b, uint4 (&d)[kNC]) {
+      unsigned long long x = b.bm | (b.bm >> 32);
+      x |= x >> 16;
+      x |= x >> 8;
+      const uint32_t cm = (uint32_t)x & 0xffu;
+#pragma unroll
+      for (int i = 0; i < kNC; ++i) {
+        const int g = lane + 32 * i;
+        const int k = g / kCR, cc = g % kCR;
+        const uint4* src = reinterpret_cast<const uint4*>(Bbytes + (int64_t)b.col[k] * row_bytes) + cc;
+        if (((cm >> k) & 1u) && !(a.flags & 4)) {
+          if constexpr (kL1) {
+            d[i] = __ldg(src);
+          } else {
+            uint4 v;
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src));
+            d[i] = v;
+          }
+        } else {
+          d[i] = make_uint4(0, 0, 0, 0);
+        }
+      }
+    };
+    auto finish = [&](const Blk& b, const uint4 (&d)[kNC]) {
+      const int s = w * SP + (int)(b.m % SP);
+      mbar_wait_t(empty + s, (uint32_t)(((b.m / SP) & 1) ^ 1), prof, 0);
+      uint8_t* stageA = sA + (size_t)s * MT * kTileBytes;
+#pragma unroll
+      for (int i = 0; i < kNC; ++i) {
+        const int g = lane + 32 * i;
+        const int k = g / kCR, cc = g % kCR;
+        const int t = cc / kChunksPerTileRow;
+        const int byte = (cc % kChunksPerTileRow) * 16;
+        *reinterpret_cast<uint4*>(stageA + t * kTileBytes + a_offset<EB>(byte >> 7, k, (byte & 127) >> 4)) = d[i];
+      }
+      // decode: bit pos = local_row * 8 + local_col, value rank = popc(bits below pos)
+      uint8_t* bop = sB + (size_t)s * kBopBytes;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int pos = lane + 32 * h;
+        const bool set = (b.bm >> pos) & 1ull;
+        const int rank = pos ? __popcll(b.bm & ((1ull << pos) - 1ull)) : 0;
+        const float va = __shfl_sync(0xffffffffu, b.v0, rank & 31);
+        const float vb = __shfl_sync(0xffffffffu, b.v1, rank & 31);
+        const float v = set ? (rank < 32 ? va : vb) : 0.f;
+        const int i = pos >> 3, k = pos & 7;
+        if constexpr (EB == 4) {
+          *(uint32_t*)(bop + (k >> 2) * 128 + i * 16 + (k & 3) * 4) = to_tf32(v);
+        } else if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
+          *(__nv_bfloat16*)(bop + i * 16 + k * 2) = __float2bfloat16_rn(v);
+        } else {
+          *(__half*)(bop + i * 16 + k * 2) = __float2half_rn(v);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full + s);
+    };
+    // two blocks in flight per warp: gather block n+1 while storing block n
+    Blk ba, bb;
+    uint4 da[kNC], db[kNC];
+    bool has_a = next(ba);
+    if (has_a) issue(ba, da);
+    while (has_a) {
+      const bool has_b = next(bb);
+      if (has_b) issue(bb, db);
+      finish(ba, da);
+      if (!has_b) break;
+      has_a = next(ba);
+      if (has_a) issue(ba, da);
+      finish(bb, db);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     const long long t_prod = clock64();
     prof.v[1] = t_prod - t_begin;
 
@@ -418,9 +473,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
         for (int32_t blk = un.z; blk < un.w; ++blk, ++m) {
           const int s = w * SP + (int)(m % SP);
           mbar_wait_t(full + s, (uint32_t)((m / SP) & 1), prof, 3);
-          // the gathered rows were written by cp.async (generic proxy) and observed through
-          // the barrier; make them visible to the tensor core's async-proxy operand reads
-          if (!(a.flags & 2)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t bdesc = umma_desc(smem_u32(sB + (size_t)s * kBopBytes), 128, 256, 0);
 #pragma unroll

@@ -11,20 +11,23 @@ namespace rsh {
 constexpr int kChunkMin = 32;   // smallest blocks-per-unit a schedule may use (sizes buffers)
 constexpr int kChunkCC = 32;    // CUDA-core path: one warp walks a unit serially
 constexpr int kChunkTC = 256;   // tensor-core path: a unit stays in one TMEM accumulator
+constexpr int kTicketMax = 64;  // windows with more chunks are reduced by the fixup kernels
+constexpr int kFixSeg = 32;     // chunks per first-level fixup segment
 constexpr int kResRows = 8;     // residual rows per unit
 constexpr int kZeroRows = 32;   // uncovered rows per unit
 
 enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
 
 // header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
-//         [5]=blocks per window unit (the fixed chunking)
+//         [5]=blocks per window unit (the fixed chunking) [6]=windows reduced by the fixup
+//         kernels (more than kTicketMax chunks) [7]=unused
 // counters: uint32 [0]=next unit [1]=warps done
 struct Sched {
   int64_t* header;
   int64_t* unit_cost;  // exclusive prefix of window-unit cost (blocks + 1), [max_units + 1]
   int64_t* unit_cost_raw;
   uint32_t* counters;
-  int32_t *head, *grp_rid, *grp_b0, *grp_b1, *grp_nch, *grp_multi, *grp_slot, *unit_base, *slot_base;
+  int32_t *head, *grp_rid, *grp_b0, *grp_b1, *grp_nch, *grp_multi, *grp_slot, *unit_base, *slot_base, *big;
   uint32_t* ticket;
   int32_t* vstart;
   uint8_t* flags;
@@ -48,6 +51,7 @@ inline size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_
   s->grp_b1 = cv.take<int32_t>(E + 1);
   s->grp_nch = cv.take<int32_t>(E + 1);
   s->grp_multi = cv.take<int32_t>(E + 1);
+  s->big = cv.take<int32_t>(E + 1);
   s->grp_slot = cv.take<int32_t>(E + 1);
   s->unit_base = cv.take<int32_t>(E + 1);
   s->slot_base = cv.take<int32_t>(E + 1);

@@ -61,6 +61,12 @@ __global__ void k_window_units(int64_t E, Sched s, int32_t chunk) {
   }
 }
 
+__global__ void k_big_flags(Sched s, int64_t E) {
+  int64_t G = s.header[0];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= E; g += (int64_t)gridDim.x * blockDim.x)
+    s.flags[g] = g < G && s.grp_nch[g] > kTicketMax;
+}
+
 __global__ void k_uncover(Sched s, int64_t n_rows, int window_size, const int32_t* __restrict__ res_row, int64_t n_res) {
   int64_t G = s.header[0];
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
@@ -149,8 +155,171 @@ __device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int3
   }
 }
 
-template <int VEC, class BT, class AccT>
-__global__ void __launch_bounds__(kThreads, 4) k_spmm_cc(SpmmArgs a) {
+constexpr int kListCap = 384;  // (col, value) entries per warp list
+
+// Stream list[beg, end) of one window row: kPF B-row gathers in flight before their FMAs.
+template <int VEC, class BT, int kPF>
+__device__ __forceinline__ void row_from_list(const SpmmArgs& a, const int2* list, int beg, int end, int f0, bool active,
+                                              float (&acc)[VEC]) {
+  const BT* B = reinterpret_cast<const BT*>(a.B);
+#pragma unroll
+  for (int t = 0; t < VEC; ++t) acc[t] = 0.f;
+  int e0 = beg;
+  for (; e0 + kPF <= end; e0 += kPF) {
+    float bv[kPF][VEC];
+    float vv[kPF];
+#pragma unroll
+    for (int p = 0; p < kPF; ++p) {
+      const int2 cv = list[e0 + p];
+      vv[p] = __int_as_float(cv.y);
+      if (active) load_vec<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv[p]);
+    }
+    if (active) {
+#pragma unroll
+      for (int p = 0; p < kPF; ++p)
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) acc[t] = fmaf(vv[p], bv[p][t], acc[t]);
+    }
+  }
+  for (; e0 < end; ++e0) {
+    const int2 cv = list[e0];
+    if (active) {
+      float bv[VEC];
+      load_vec<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) acc[t] = fmaf(__int_as_float(cv.y), bv[t], acc[t]);
+    }
+  }
+}
+
+// fp32 window unit, walked ROW by row.  The unit's (<= 32) blocks are listed once as (col,
+// value) pairs in shared memory, grouped by window row -- lane l owns block l; packed warp scans
+// of the per-row popcounts place every entry, and each lane only visits its set bits -- then
+// each row streams its segment with kPF gathers in flight.  One accumulator row (VEC registers)
+// instead of eight leaves the registers for gathers in flight; the accumulation order (blocks in
+// order, columns in order within a block) is the block walk's.  Units with more than kListCap
+// nonzeros are listed one row at a time.
+template <int VEC, class BT, int kPF>
+__device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t rid, int64_t avail, int32_t slot,
+                                            int32_t k, int n_fc, int2* list, int* tab) {
+  const int lane = threadIdx.x & 31;
+  const int32_t b0 = un.z, b1 = un.w;
+  const int32_t blk = b0 + lane;
+  const bool mine = blk < b1;
+  const unsigned long long bm = mine ? __ldg(a.bitmaps + blk) : 0ull;
+  const int32_t vs = mine ? __ldg(a.s.vstart + blk) : 0;
+  const int nrows = slot < 0 ? (int)avail : 8;
+  // per-row counts of this lane's block, packed 4 rows x 16 bits per word
+  unsigned long long p0 = 0, p1 = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    p0 |= (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
+    p1 |= (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
+  }
+  unsigned long long q0 = p0, q1 = p1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t0 = __shfl_up_sync(0xffffffffu, q0, o);
+    const unsigned long long t1 = __shfl_up_sync(0xffffffffu, q1, o);
+    if (lane >= o) {
+      q0 += t0;
+      q1 += t1;
+    }
+  }
+  const unsigned long long tot0 = __shfl_sync(0xffffffffu, q0, 31), tot1 = __shfl_sync(0xffffffffu, q1, 31);
+  // inclusive prefix over rows of the row totals (fields never overflow 16 bits)
+  const unsigned long long rp0 = tot0 * 0x0001000100010001ull;
+  const unsigned long long rp1 = tot1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
+  const int total = (int)(rp1 >> 48);
+  auto row_end = [&](int i) -> int {
+    return (int)(((i < 4 ? rp0 : rp1) >> (16 * (i & 3))) & 0xffffull);
+  };
+  if (total <= kListCap) {
+    const unsigned long long e0 = q0 - p0, e1 = q1 - p1;  // exclusive lane prefixes
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row_beg = i ? row_end(i - 1) : 0;
+      const int lane_off = (int)(((i < 4 ? e0 : e1) >> (16 * (i & 3))) & 0xffffull);
+      tab[lane * 8 + i] = row_beg + lane_off;
+    }
+    __syncwarp();
+    unsigned long long rem = bm;
+    int vrank = 0;
+    while (rem) {
+      const int bit = __ffsll((long long)rem) - 1;
+      rem &= rem - 1;
+      const int i = bit >> 3, j = bit & 7;
+      const uint32_t byte = uint32_t(bm >> (8 * i)) & 0xffu;
+      const int pos = tab[lane * 8 + i] + __popc(byte & ((1u << j) - 1u));
+      list[pos] = make_int2(__ldg(a.col_id + (int64_t)blk * 8 + j), __float_as_int(__ldg(a.tc_values + vs + vrank)));
+      ++vrank;
+    }
+    __syncwarp();
+    for (int i = 0; i < nrows; ++i) {
+      const int beg = i ? row_end(i - 1) : 0, end = row_end(i);
+      for (int fc = 0; fc < n_fc; ++fc) {
+        const int f0 = fc * 32 * VEC + lane * VEC;
+        const bool active = f0 < a.N;
+        float acc[VEC];
+        row_from_list<VEC, BT, kPF>(a, list, beg, end, f0, active, acc);
+        if (active) {
+          if (slot < 0) {
+            store_c<VEC, float>(a.C + (rid + i) * a.ldc + f0, acc);
+          } else {
+            float* part = reinterpret_cast<float*>(a.partials) + ((int64_t)(slot + k) * 8 + i) * a.N + f0;
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) __stcg(part + t, acc[t]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  // dense unit: one row at a time (each row has at most 32 x 8 = 256 entries)
+  for (int i = 0; i < nrows; ++i) {
+    const uint32_t byte = uint32_t(bm >> (8 * i)) & 0xffu;
+    const int cnt = __popc(byte);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int rtotal = __shfl_sync(0xffffffffu, incl, 31);
+    int pos = incl - cnt;
+    int vrank = i ? __popcll(bm & ((1ull << (8 * i)) - 1ull)) : 0;
+    uint32_t rb = byte;
+    while (rb) {
+      const int j = __ffs(rb) - 1;
+      rb &= rb - 1;
+      list[pos++] = make_int2(__ldg(a.col_id + (int64_t)blk * 8 + j), __float_as_int(__ldg(a.tc_values + vs + vrank)));
+      ++vrank;
+    }
+    __syncwarp();
+    for (int fc = 0; fc < n_fc; ++fc) {
+      const int f0 = fc * 32 * VEC + lane * VEC;
+      const bool active = f0 < a.N;
+      float acc[VEC];
+      row_from_list<VEC, BT, kPF>(a, list, 0, rtotal, f0, active, acc);
+      if (active) {
+        if (slot < 0) {
+          store_c<VEC, float>(a.C + (rid + i) * a.ldc + f0, acc);
+        } else {
+          float* part = reinterpret_cast<float*>(a.partials) + ((int64_t)(slot + k) * 8 + i) * a.N + f0;
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) __stcg(part + t, acc[t]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int VEC, class BT, class AccT, int MINB = 4, int PF = 4>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_cc(SpmmArgs a) {
+  __shared__ int2 s_list[kThreads / 32][kListCap];  // per-warp (col, value) list of a window unit
+  __shared__ int s_tab[kThreads / 32][256];          // per-warp list offsets (lane, row)
   const int lane = threadIdx.x & 31;
   const int64_t total_units = a.s.header[2];
   const int n_fc = (a.N + 32 * VEC - 1) / (32 * VEC);
@@ -167,6 +336,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmm_cc(SpmmArgs a) {
       int64_t rid = a.s.grp_rid[g];
       int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
       int32_t slot = a.s.grp_slot[g];
+      if constexpr (std::is_same<AccT, float>::value) {
+        window_rows<VEC, BT, PF>(a, un, rid, avail, slot, k, n_fc, s_list[threadIdx.x >> 5], s_tab[threadIdx.x >> 5]);
+      } else
       for (int fc = 0; fc < n_fc; ++fc) {
         int f0 = fc * 32 * VEC + lane * VEC;
         bool active = f0 < a.N;
@@ -186,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmm_cc(SpmmArgs a) {
             for (int t = 0; t < VEC; ++t) __stcg(part + (int64_t)i * a.N + f0 + t, acc[i][t]);
         }
       }
-      if (slot >= 0) {
+      if (slot >= 0 && a.s.grp_nch[g] <= kTicketMax) {
         __threadfence();
         __syncwarp();
         uint32_t t = 0;
@@ -256,18 +428,98 @@ __global__ void k_max_rel(const float* __restrict__ c, const float* __restrict__
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
-template <int VEC, class BT, class AccT>
-int launch_cc(const SpmmArgs& a, cudaStream_t st) {
+// ------------------------------------------------------------------------------------------
+// fixup of very long windows: partials of windows with more than kTicketMax chunks are summed
+// by the whole GPU in a fixed two-level order (segments of kFixSeg chunks, then segments), so the
+// result stays deterministic and independent of the format's split segments.
+// ------------------------------------------------------------------------------------------
+
+template <class AccT>
+__global__ void k_fixup_segments(SpmmArgs a) {
+  const int64_t nbig = a.s.header[6];
+  const int64_t N = a.N;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  AccT* P = reinterpret_cast<AccT*>(a.partials);
+  for (int64_t gi = 0; gi < nbig; ++gi) {
+    const int32_t g = a.s.big[gi];
+    const int32_t nch = a.s.grp_nch[g], slot = a.s.grp_slot[g];
+    const int64_t nseg = (nch + kFixSeg - 1) / kFixSeg;
+    for (int64_t t = tid; t < nseg * 8 * N; t += stride) {
+      const int64_t f = t % N, i = (t / N) % 8, seg = t / (8 * N);
+      const int c0 = (int)seg * kFixSeg, c1 = c0 + kFixSeg < nch ? c0 + kFixSeg : nch;
+      const AccT* src = P + ((int64_t)slot * 8 + i) * N + f;
+      AccT sum = AccT(0);
+      int c = c0;
+      for (; c + 8 <= c1; c += 8) {
+        AccT v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(c + u) * 8 * N);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += v[u];
+      }
+      for (; c < c1; ++c) sum += __ldcg(src + (int64_t)c * 8 * N);
+      __stcg(P + ((int64_t)(slot + c0) * 8 + i) * N + f, sum);
+    }
+  }
+}
+
+template <class AccT>
+__global__ void k_fixup_rows(SpmmArgs a) {
+  const int64_t nbig = a.s.header[6];
+  const int64_t N = a.N;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  const AccT* P = reinterpret_cast<const AccT*>(a.partials);
+  for (int64_t gi = 0; gi < nbig; ++gi) {
+    const int32_t g = a.s.big[gi];
+    const int32_t nch = a.s.grp_nch[g], slot = a.s.grp_slot[g];
+    const int64_t rid = a.s.grp_rid[g];
+    const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
+    const int nseg = (nch + kFixSeg - 1) / kFixSeg;
+    for (int64_t t = tid; t < avail * N; t += stride) {
+      const int64_t f = t % N, i = t / N;
+      AccT sum = AccT(0);
+      for (int sg = 0; sg < nseg; ++sg) sum += __ldcg(P + ((int64_t)(slot + sg * kFixSeg) * 8 + i) * N + f);
+      __stcs(a.C + (rid + i) * a.ldc + f, (float)sum);
+    }
+  }
+}
+
+template <class AccT>
+int launch_fixup(const SpmmArgs& a, cudaStream_t st) {
+  const unsigned blocks = (unsigned)(2 * sm_count());
+  k_fixup_segments<AccT><<<blocks, kThreads, 0, st>>>(a);
+  k_fixup_rows<AccT><<<blocks, kThreads, 0, st>>>(a);
+  RSH_LAUNCHED("k_fixup");
+  return kOk;
+}
+template int launch_fixup<float>(const SpmmArgs&, cudaStream_t);
+
+template <int VEC, class BT, class AccT, int MINB, int PF>
+int launch_cc_v(const SpmmArgs& a, cudaStream_t st) {
   static int blocks = 0;
+  auto kern = k_spmm_cc<VEC, BT, AccT, MINB, PF>;
   if (!blocks) {
     int per_sm = 0;
-    RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm_cc<VEC, BT, AccT>, kThreads, 0));
-    RSH_CUDA(cudaFuncSetAttribute(k_spmm_cc<VEC, BT, AccT>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
     blocks = (per_sm > 0 ? per_sm : 1) * sm_count();
   }
-  k_spmm_cc<VEC, BT, AccT><<<blocks, kThreads, 0, st>>>(a);
+  kern<<<blocks, kThreads, 0, st>>>(a);
   RSH_LAUNCHED("k_spmm_cc");
-  return kOk;
+  return launch_fixup<AccT>(a, st);
+}
+
+template <int VEC, class BT, class AccT>
+int launch_cc(const SpmmArgs& a, cudaStream_t st) {
+  if constexpr (std::is_same<AccT, float>::value && VEC == 4) {
+    // occupancy / gathers-in-flight trade-off (tuning knob, flags bits 1-2)
+    switch (a.flags & 3) {
+      case 1: return launch_cc_v<VEC, BT, AccT, 3, 8>(a, st);
+      case 2: return launch_cc_v<VEC, BT, AccT, 4, 8>(a, st);
+      case 3: return launch_cc_v<VEC, BT, AccT, 4, 4>(a, st);
+      default: break;
+    }
+  }
+  return launch_cc_v<VEC, BT, AccT, 3, 4>(a, st);
 }
 
 template <class BT, class AccT>
@@ -332,6 +584,12 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   }
   cb = s.cub_bytes;
   RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.unit_cost_raw, s.unit_cost, (int)(s.max_units + 1), st));
+  // windows with more than kTicketMax chunks: reduced by the fixup kernels, not by tickets
+  k_big_flags<<<grid_1d(E + 1), kThreads, 0, st>>>(s, E);
+  RSH_LAUNCHED("k_big_flags");
+  cb = s.cub_bytes;
+  RSH_CUDA(cub::DeviceSelect::Flagged(s.cub, cb, cub::CountingInputIterator<int32_t>(0), s.flags, s.big,
+                                      s.header + 6, (int)(E + 1), st));
   // per-block value starts (execute.py:167-168)
   k_popc32<<<grid_1d(n_blocks + 1), kThreads, 0, st>>>((const unsigned long long*)bitmaps, n_blocks, s.pc);
   cb = s.cub_bytes;
@@ -365,7 +623,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 1) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 7) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -386,7 +644,8 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.window_size = window_size;
   a.s = s;
   a.partials = partials;
-  a.flags = 0;
+  a.flags = accum >> 1;  // tuning knob: CUDA-core occupancy variant
+  accum &= 1;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;
   int vec = 8;

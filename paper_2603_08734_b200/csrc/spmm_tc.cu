@@ -22,6 +22,8 @@
 #include "sched.cuh"
 
 namespace rsh {
+template <class AccT>
+int launch_fixup(const SpmmArgs& a, cudaStream_t st);  // spmm_cc.cu
 namespace tc {
 
 constexpr int kPipes = 4;        // independent producer -> MMA pipelines per CTA
@@ -541,9 +543,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) __stcg(part + (int64_t)i * a.N + t * 128 + f_in_tile, r[t][i]);
         // one thread publishes for the whole epilogue group (bar.sync orders the others' stores
-        // before its fence) and, if it took the last ticket, acquires for everyone
+        // before its fence) and, if it took the last ticket, acquires for everyone; windows
+        // with more than kTicketMax chunks are left to the fixup kernels
         const long long tp = prof.on ? clock64() : 0;
         const int32_t nch = a.s.grp_nch[g];
+        if (nch > kTicketMax) continue;
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
         if (threadIdx.x == 0) {
           __threadfence();
@@ -611,7 +615,7 @@ int launch(const SpmmArgs& a, cudaStream_t st) {
   }
   kern<<<sm_count(), kThreadsTC, bytes, st>>>(a);
   RSH_LAUNCHED("k_spmm_tc");
-  return kOk;
+  return launch_fixup<float>(a, st);
 }
 
 }  // namespace tc

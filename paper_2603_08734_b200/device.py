@@ -337,7 +337,7 @@ def resolve_math(math: str, b: torch.Tensor, t: DeviceTile, accumulate: str) -> 
 
 
 def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None, accumulate: str = "f32",
-                stream=None, math: str = "auto", l1: bool = True) -> torch.Tensor:
+                stream=None, math: str = "auto", l1: bool = True, cc_variant: int = 0) -> torch.Tensor:
     """C = A @ B with A an RS-Tile on device; B [n_cols, N] f32/bf16/f16 row-major on device.
     Returns (or fills) C [n_rows, N] float32.  accumulate: "f32" | "f64" (execute.py:33-49);
     math: "auto" | "fp32" (CUDA-core FMA) | "tf32" (tensor cores, see resolve_math)."""
@@ -363,7 +363,7 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
     call("rsh_spmm_tc" if path == "tc" else "rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
          _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),
          _ptr(t.res_values), t.n_res, _ptr(b), b.stride(0), _BDT[b.dtype], N, _ptr(out), out.stride(0),
-         int(l1) if path == "tc" else acc, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
+         int(l1) if path == "tc" else acc | (cc_variant << 1), _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
     return out
 
 

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--math", default="auto")
     ap.add_argument("--l1", type=int, default=1)
+    ap.add_argument("--ccv", type=int, default=0)
     ap.add_argument("--ccflags", type=int, default=0)
     args = ap.parse_args()
     t0 = time.time()
@@ -54,14 +55,14 @@ def main():
     out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(3):
-        spmm_device(t, bt, out=out, math=args.math, l1=args.l1)
+        spmm_device(t, bt, out=out, math=args.math, l1=args.l1, cc_variant=args.ccv)
     torch.cuda.synchronize()
     times = []
     for _ in range(args.iters):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        spmm_device(t, bt, out=out, math=args.math, l1=args.l1)
+        spmm_device(t, bt, out=out, math=args.math, l1=args.l1, cc_variant=args.ccv)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))

@@ -34,7 +34,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SpMM GFLOP/s (2*nnz*N/t)"
-GATHER_ROOF_GBS = 6772.0  # profiles/r01_gather_bw_microbench.txt: L2-resident random 512-B rows
+# profiles/r01_gather_bw2_microbench.txt: random 512-B B rows gathered with LDG.128 by 148 SMs
+GATHER_ROOF_L2_GBS = 18454.0   # 64 MB footprint (L2-resident)
+GATHER_ROOF_HBM_GBS = 7291.0   # 2 GB footprint (from HBM)
 
 
 def _peaks() -> dict:
@@ -49,8 +51,9 @@ def _traffic(workload: str):
     """dram read+write bytes per launch of the SpMM kernel from the committed ncu capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            return json.load(fh).get(workload)
-    except OSError:
+            rec = json.load(fh).get(workload)
+        return None if rec is None else rec["dram_bytes_per_launch"]
+    except (OSError, KeyError, TypeError):
         return None
 
 
@@ -372,8 +375,10 @@ def run_single(args):
                      "algorithmic_bytes": alg_bytes, "kernel": kernel, "kernel_ms": kern_avg,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
         "gather": {"gathered_bytes": gathered, "achieved_gbs": gathered / (kern_avg * 1e-3) / 1e9,
-                   "roof_gbs": GATHER_ROOF_GBS,
-                   "frac": gathered / (kern_avg * 1e-3) / 1e9 / GATHER_ROOF_GBS},
+                   "roof_l2_resident_gbs": GATHER_ROOF_L2_GBS, "roof_hbm_gbs": GATHER_ROOF_HBM_GBS,
+                   "frac_of_l2_roof": gathered / (kern_avg * 1e-3) / 1e9 / GATHER_ROOF_L2_GBS,
+                   "note": "B rows the window path must move into the SMs (one per occupied col_id slot "
+                           "+ one per residual nonzero); roofs measured by tools/microbench/gather_bw2.cu"},
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms)),
                 "path": f"{kernel} via the C ABI (ctypes), pinned host format + B in, C out"},

@@ -20,7 +20,7 @@ enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
 
 // header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
 //         [5]=blocks per window unit (the fixed chunking) [6]=windows reduced by the fixup
-//         kernels (more than kTicketMax chunks) [7]=unused
+//         kernels (more than kTicketMax chunks) [7]=their first-level fix-up segments
 // counters: uint32 [0]=next unit [1]=warps done
 struct Sched {
   int64_t* header;
@@ -28,6 +28,7 @@ struct Sched {
   int64_t* unit_cost_raw;
   uint32_t* counters;
   int32_t *head, *grp_rid, *grp_b0, *grp_b1, *grp_nch, *grp_multi, *grp_slot, *unit_base, *slot_base, *big;
+  int32_t* seg_base;  // exclusive prefix of fix-up segments over the big windows
   uint32_t* ticket;
   int32_t* vstart;
   uint8_t* flags;
@@ -52,6 +53,7 @@ inline size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_
   s->grp_nch = cv.take<int32_t>(E + 1);
   s->grp_multi = cv.take<int32_t>(E + 1);
   s->big = cv.take<int32_t>(E + 1);
+  s->seg_base = cv.take<int32_t>(E + 2);
   s->grp_slot = cv.take<int32_t>(E + 1);
   s->unit_base = cv.take<int32_t>(E + 1);
   s->slot_base = cv.take<int32_t>(E + 1);
@@ -116,6 +118,52 @@ __device__ __forceinline__ void load_vec(const BT* __restrict__ p, float (&o)[VE
   } else {
 #pragma unroll
     for (int t = 0; t < VEC; ++t) o[t] = to_f<BT>(p[t]);
+  }
+}
+
+// L2 cache policies: B rows are the reused operand (evict_last), the format stream is read once
+// (evict_first)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ldg_hint(const void* p, uint64_t pol) {
+  uint4 u;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p), "l"(pol));
+  return u;
+}
+__device__ __forceinline__ uint32_t ldg_hint32(const void* p, uint64_t pol) {
+  uint32_t u;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(u) : "l"(p), "l"(pol));
+  return u;
+}
+__device__ __forceinline__ unsigned long long ldg_hint64(const void* p, uint64_t pol) {
+  unsigned long long u;
+  asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(u) : "l"(p), "l"(pol));
+  return u;
+}
+
+// load_vec with an L2 policy (16-byte multiples; other widths fall back to load_vec)
+template <int VEC, class BT>
+__device__ __forceinline__ void load_vec_pol(const BT* __restrict__ p, float (&o)[VEC], uint64_t pol) {
+  constexpr int bytes = VEC * (int)sizeof(BT);
+  if constexpr (bytes % 16 == 0) {
+#pragma unroll
+    for (int q = 0; q < bytes / 16; ++q) {
+      uint4 u = ldg_hint(reinterpret_cast<const uint4*>(p) + q, pol);
+      const BT* e = reinterpret_cast<const BT*>(&u);
+#pragma unroll
+      for (int t = 0; t < 16 / (int)sizeof(BT); ++t) o[q * (16 / sizeof(BT)) + t] = to_f<BT>(e[t]);
+    }
+  } else {
+    load_vec<VEC, BT>(p, o);
   }
 }
 

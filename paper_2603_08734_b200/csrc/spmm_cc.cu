@@ -67,6 +67,18 @@ __global__ void k_big_flags(Sched s, int64_t E) {
     s.flags[g] = g < G && s.grp_nch[g] > kTicketMax;
 }
 
+// first-level fix-up segments of the big windows (few windows: one thread)
+__global__ void k_seg_base(Sched s) {
+  const int64_t nbig = s.header[6];
+  int32_t acc = 0;
+  for (int64_t i = 0; i < nbig; ++i) {
+    s.seg_base[i] = acc;
+    acc += (s.grp_nch[s.big[i]] + kFixSeg - 1) / kFixSeg;
+  }
+  s.seg_base[nbig] = acc;
+  s.header[7] = acc;
+}
+
 __global__ void k_uncover(Sched s, int64_t n_rows, int window_size, const int32_t* __restrict__ res_row, int64_t n_res) {
   int64_t G = s.header[0];
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
@@ -160,7 +172,7 @@ constexpr int kListCap = 384;  // (col, value) entries per warp list
 // Stream list[beg, end) of one window row: kPF B-row gathers in flight before their FMAs.
 template <int VEC, class BT, int kPF>
 __device__ __forceinline__ void row_from_list(const SpmmArgs& a, const int2* list, int beg, int end, int f0, bool active,
-                                              float (&acc)[VEC]) {
+                                              float (&acc)[VEC], uint64_t pol) {
   const BT* B = reinterpret_cast<const BT*>(a.B);
 #pragma unroll
   for (int t = 0; t < VEC; ++t) acc[t] = 0.f;
@@ -172,7 +184,7 @@ __device__ __forceinline__ void row_from_list(const SpmmArgs& a, const int2* lis
     for (int p = 0; p < kPF; ++p) {
       const int2 cv = list[e0 + p];
       vv[p] = __int_as_float(cv.y);
-      if (active) load_vec<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv[p]);
+      if (active) load_vec_pol<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv[p], pol);
     }
     if (active) {
 #pragma unroll
@@ -185,7 +197,7 @@ __device__ __forceinline__ void row_from_list(const SpmmArgs& a, const int2* lis
     const int2 cv = list[e0];
     if (active) {
       float bv[VEC];
-      load_vec<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv);
+      load_vec_pol<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv, pol);
 #pragma unroll
       for (int t = 0; t < VEC; ++t) acc[t] = fmaf(__int_as_float(cv.y), bv[t], acc[t]);
     }
@@ -206,9 +218,20 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
   const int32_t b0 = un.z, b1 = un.w;
   const int32_t blk = b0 + lane;
   const bool mine = blk < b1;
-  const unsigned long long bm = mine ? __ldg(a.bitmaps + blk) : 0ull;
+  // L2 policy: B rows evict_last (reused across windows), the format stream evict_first
+  const bool hints = !(a.flags & 4);
+  const uint64_t pol_b = hints ? policy_evict_last() : 0, pol_a = hints ? policy_evict_first() : 0;
+  const unsigned long long bm = mine ? (hints ? ldg_hint64(a.bitmaps + blk, pol_a) : __ldg(a.bitmaps + blk)) : 0ull;
   const int32_t vs = mine ? __ldg(a.s.vstart + blk) : 0;
   const int nrows = slot < 0 ? (int)avail : 8;
+  auto meta_col = [&](int j) -> int32_t {
+    const int32_t* p = a.col_id + (int64_t)blk * 8 + j;
+    return hints ? (int32_t)ldg_hint32(p, pol_a) : __ldg(p);
+  };
+  auto meta_val = [&](int r) -> int32_t {
+    const float* p = a.tc_values + vs + r;
+    return hints ? (int32_t)ldg_hint32(p, pol_a) : __float_as_int(__ldg(p));
+  };
   // per-row counts of this lane's block, packed 4 rows x 16 bits per word
   unsigned long long p0 = 0, p1 = 0;
 #pragma unroll
@@ -251,7 +274,7 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
       const int i = bit >> 3, j = bit & 7;
       const uint32_t byte = uint32_t(bm >> (8 * i)) & 0xffu;
       const int pos = tab[lane * 8 + i] + __popc(byte & ((1u << j) - 1u));
-      list[pos] = make_int2(__ldg(a.col_id + (int64_t)blk * 8 + j), __float_as_int(__ldg(a.tc_values + vs + vrank)));
+      list[pos] = make_int2(meta_col(j), meta_val(vrank));
       ++vrank;
     }
     __syncwarp();
@@ -261,7 +284,7 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
         const int f0 = fc * 32 * VEC + lane * VEC;
         const bool active = f0 < a.N;
         float acc[VEC];
-        row_from_list<VEC, BT, kPF>(a, list, beg, end, f0, active, acc);
+        row_from_list<VEC, BT, kPF>(a, list, beg, end, f0, active, acc, pol_b);
         if (active) {
           if (slot < 0) {
             store_c<VEC, float>(a.C + (rid + i) * a.ldc + f0, acc);
@@ -293,7 +316,7 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
     while (rb) {
       const int j = __ffs(rb) - 1;
       rb &= rb - 1;
-      list[pos++] = make_int2(__ldg(a.col_id + (int64_t)blk * 8 + j), __float_as_int(__ldg(a.tc_values + vs + vrank)));
+      list[pos++] = make_int2(meta_col(j), meta_val(vrank));
       ++vrank;
     }
     __syncwarp();
@@ -301,7 +324,7 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
       const int f0 = fc * 32 * VEC + lane * VEC;
       const bool active = f0 < a.N;
       float acc[VEC];
-      row_from_list<VEC, BT, kPF>(a, list, 0, rtotal, f0, active, acc);
+      row_from_list<VEC, BT, kPF>(a, list, 0, rtotal, f0, active, acc, pol_b);
       if (active) {
         if (slot < 0) {
           store_c<VEC, float>(a.C + (rid + i) * a.ldc + f0, acc);
@@ -436,30 +459,32 @@ __global__ void k_max_rel(const float* __restrict__ c, const float* __restrict__
 
 template <class AccT>
 __global__ void k_fixup_segments(SpmmArgs a) {
-  const int64_t nbig = a.s.header[6];
+  const int64_t nbig = a.s.header[6], nsegs = a.s.header[7];
   const int64_t N = a.N;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   AccT* P = reinterpret_cast<AccT*>(a.partials);
-  for (int64_t gi = 0; gi < nbig; ++gi) {
-    const int32_t g = a.s.big[gi];
-    const int32_t nch = a.s.grp_nch[g], slot = a.s.grp_slot[g];
-    const int64_t nseg = (nch + kFixSeg - 1) / kFixSeg;
-    for (int64_t t = tid; t < nseg * 8 * N; t += stride) {
-      const int64_t f = t % N, i = (t / N) % 8, seg = t / (8 * N);
-      const int c0 = (int)seg * kFixSeg, c1 = c0 + kFixSeg < nch ? c0 + kFixSeg : nch;
-      const AccT* src = P + ((int64_t)slot * 8 + i) * N + f;
-      AccT sum = AccT(0);
-      int c = c0;
-      for (; c + 8 <= c1; c += 8) {
-        AccT v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(c + u) * 8 * N);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) sum += v[u];
-      }
-      for (; c < c1; ++c) sum += __ldcg(src + (int64_t)c * 8 * N);
-      __stcg(P + ((int64_t)(slot + c0) * 8 + i) * N + f, sum);
+  for (int64_t t = tid; t < nsegs * 8 * N; t += stride) {
+    const int64_t f = t % N, i = (t / N) % 8, sg = t / (8 * N);
+    int64_t lo = 0, hi = nbig - 1;  // big window owning global segment sg
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (a.s.seg_base[mid] <= sg) lo = mid; else hi = mid - 1;
     }
+    const int32_t g = a.s.big[lo];
+    const int32_t nch = a.s.grp_nch[g], slot = a.s.grp_slot[g];
+    const int c0 = (int)(sg - a.s.seg_base[lo]) * kFixSeg, c1 = c0 + kFixSeg < nch ? c0 + kFixSeg : nch;
+    const AccT* src = P + ((int64_t)slot * 8 + i) * N + f;
+    AccT sum = AccT(0);
+    int c = c0;
+    for (; c + 8 <= c1; c += 8) {
+      AccT v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(c + u) * 8 * N);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; c < c1; ++c) sum += __ldcg(src + (int64_t)c * 8 * N);
+    __stcg(P + ((int64_t)(slot + c0) * 8 + i) * N + f, sum);
   }
 }
 
@@ -469,18 +494,17 @@ __global__ void k_fixup_rows(SpmmArgs a) {
   const int64_t N = a.N;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   const AccT* P = reinterpret_cast<const AccT*>(a.partials);
-  for (int64_t gi = 0; gi < nbig; ++gi) {
+  for (int64_t t = tid; t < nbig * 8 * N; t += stride) {
+    const int64_t f = t % N, i = (t / N) % 8, gi = t / (8 * N);
     const int32_t g = a.s.big[gi];
-    const int32_t nch = a.s.grp_nch[g], slot = a.s.grp_slot[g];
     const int64_t rid = a.s.grp_rid[g];
     const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
+    if (i >= avail) continue;
+    const int32_t nch = a.s.grp_nch[g], slot = a.s.grp_slot[g];
     const int nseg = (nch + kFixSeg - 1) / kFixSeg;
-    for (int64_t t = tid; t < avail * N; t += stride) {
-      const int64_t f = t % N, i = t / N;
-      AccT sum = AccT(0);
-      for (int sg = 0; sg < nseg; ++sg) sum += __ldcg(P + ((int64_t)(slot + sg * kFixSeg) * 8 + i) * N + f);
-      __stcs(a.C + (rid + i) * a.ldc + f, (float)sum);
-    }
+    AccT sum = AccT(0);
+    for (int sg = 0; sg < nseg; ++sg) sum += __ldcg(P + ((int64_t)(slot + sg * kFixSeg) * 8 + i) * N + f);
+    __stcs(a.C + (rid + i) * a.ldc + f, (float)sum);
   }
 }
 
@@ -590,6 +614,8 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   cb = s.cub_bytes;
   RSH_CUDA(cub::DeviceSelect::Flagged(s.cub, cb, cub::CountingInputIterator<int32_t>(0), s.flags, s.big,
                                       s.header + 6, (int)(E + 1), st));
+  k_seg_base<<<1, 1, 0, st>>>(s);
+  RSH_LAUNCHED("k_seg_base");
   // per-block value starts (execute.py:167-168)
   k_popc32<<<grid_1d(n_blocks + 1), kThreads, 0, st>>>((const unsigned long long*)bitmaps, n_blocks, s.pc);
   cb = s.cub_bytes;
@@ -623,7 +649,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 7) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 15) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -644,7 +670,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.window_size = window_size;
   a.s = s;
   a.partials = partials;
-  a.flags = accum >> 1;  // tuning knob: CUDA-core occupancy variant
+  a.flags = accum >> 1;  // tuning knobs: bits 0-1 occupancy variant, bit 2 no L2 cache hints
   accum &= 1;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;

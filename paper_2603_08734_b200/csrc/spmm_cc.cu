@@ -170,19 +170,24 @@ __device__ __forceinline__ void window_chunk(const SpmmArgs& a, int32_t b0, int3
 constexpr int kListCap = 384;  // (col, value) entries per warp list
 
 // Stream list[beg, end) of one window row: kPF B-row gathers in flight before their FMAs.
-template <int VEC, class BT, int kPF>
+// Stream list[beg, end) of one window row with kPF B-row gathers in flight before their FMAs.
+// G > 1 (narrow rows, N = 128 / G fp32 features): the warp splits into G lane groups that take
+// alternate entries with full 16-byte loads, and the G partial sums are combined by a fixed
+// xor-shuffle tree at the end (deterministic).
+template <int VEC, class BT, int kPF, int G>
 __device__ __forceinline__ void row_from_list(const SpmmArgs& a, const int2* list, int beg, int end, int f0, bool active,
                                               float (&acc)[VEC], uint64_t pol) {
   const BT* B = reinterpret_cast<const BT*>(a.B);
+  const int grp = G > 1 ? (int)(threadIdx.x & 31) / (32 / G) : 0;
 #pragma unroll
   for (int t = 0; t < VEC; ++t) acc[t] = 0.f;
   int e0 = beg;
-  for (; e0 + kPF <= end; e0 += kPF) {
+  for (; e0 + kPF * G <= end; e0 += kPF * G) {
     float bv[kPF][VEC];
     float vv[kPF];
 #pragma unroll
     for (int p = 0; p < kPF; ++p) {
-      const int2 cv = list[e0 + p];
+      const int2 cv = list[e0 + p * G + grp];
       vv[p] = __int_as_float(cv.y);
       if (active) load_vec_pol<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv[p], pol);
     }
@@ -193,14 +198,20 @@ __device__ __forceinline__ void row_from_list(const SpmmArgs& a, const int2* lis
         for (int t = 0; t < VEC; ++t) acc[t] = fmaf(vv[p], bv[p][t], acc[t]);
     }
   }
-  for (; e0 < end; ++e0) {
-    const int2 cv = list[e0];
+  for (int e = e0 + grp; e < end; e += G) {
+    const int2 cv = list[e];
     if (active) {
       float bv[VEC];
       load_vec_pol<VEC, BT>(B + (int64_t)cv.x * a.ldb + f0, bv, pol);
 #pragma unroll
       for (int t = 0; t < VEC; ++t) acc[t] = fmaf(__int_as_float(cv.y), bv[t], acc[t]);
     }
+  }
+  if constexpr (G > 1) {
+#pragma unroll
+    for (int off = 16; off >= 32 / G; off >>= 1)
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], off);
   }
 }
 
@@ -211,7 +222,7 @@ __device__ __forceinline__ void row_from_list(const SpmmArgs& a, const int2* lis
 // instead of eight leaves the registers for gathers in flight; the accumulation order (blocks in
 // order, columns in order within a block) is the block walk's.  Units with more than kListCap
 // nonzeros are listed one row at a time.
-template <int VEC, class BT, int kPF>
+template <int VEC, class BT, int kPF, int G>
 __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t rid, int64_t avail, int32_t slot,
                                             int32_t k, int n_fc, int2* list, int* tab) {
   const int lane = threadIdx.x & 31;
@@ -281,11 +292,11 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
     for (int i = 0; i < nrows; ++i) {
       const int beg = i ? row_end(i - 1) : 0, end = row_end(i);
       for (int fc = 0; fc < n_fc; ++fc) {
-        const int f0 = fc * 32 * VEC + lane * VEC;
+        const int f0 = G > 1 ? (lane % (32 / G)) * VEC : fc * 32 * VEC + lane * VEC;
         const bool active = f0 < a.N;
         float acc[VEC];
-        row_from_list<VEC, BT, kPF>(a, list, beg, end, f0, active, acc, pol_b);
-        if (active) {
+        row_from_list<VEC, BT, kPF, G>(a, list, beg, end, f0, active, acc, pol_b);
+        if (active && (G == 1 || lane < 32 / G)) {
           if (slot < 0) {
             store_c<VEC, float>(a.C + (rid + i) * a.ldc + f0, acc);
           } else {
@@ -321,11 +332,11 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
     }
     __syncwarp();
     for (int fc = 0; fc < n_fc; ++fc) {
-      const int f0 = fc * 32 * VEC + lane * VEC;
+      const int f0 = G > 1 ? (lane % (32 / G)) * VEC : fc * 32 * VEC + lane * VEC;
       const bool active = f0 < a.N;
       float acc[VEC];
-      row_from_list<VEC, BT, kPF>(a, list, 0, rtotal, f0, active, acc, pol_b);
-      if (active) {
+      row_from_list<VEC, BT, kPF, G>(a, list, 0, rtotal, f0, active, acc, pol_b);
+      if (active && (G == 1 || lane < 32 / G)) {
         if (slot < 0) {
           store_c<VEC, float>(a.C + (rid + i) * a.ldc + f0, acc);
         } else {
@@ -339,7 +350,7 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
   }
 }
 
-template <int VEC, class BT, class AccT, int MINB = 4, int PF = 4>
+template <int VEC, class BT, class AccT, int MINB = 4, int PF = 4, int G = 1>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_cc(SpmmArgs a) {
   __shared__ int2 s_list[kThreads / 32][kListCap];  // per-warp (col, value) list of a window unit
   __shared__ int s_tab[kThreads / 32][256];          // per-warp list offsets (lane, row)
@@ -360,7 +371,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_cc(SpmmArgs a) {
       int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
       int32_t slot = a.s.grp_slot[g];
       if constexpr (std::is_same<AccT, float>::value) {
-        window_rows<VEC, BT, PF>(a, un, rid, avail, slot, k, n_fc, s_list[threadIdx.x >> 5], s_tab[threadIdx.x >> 5]);
+        window_rows<VEC, BT, PF, G>(a, un, rid, avail, slot, k, G > 1 ? 1 : n_fc, s_list[threadIdx.x >> 5],
+                                   s_tab[threadIdx.x >> 5]);
       } else
       for (int fc = 0; fc < n_fc; ++fc) {
         int f0 = fc * 32 * VEC + lane * VEC;
@@ -518,10 +530,10 @@ int launch_fixup(const SpmmArgs& a, cudaStream_t st) {
 }
 template int launch_fixup<float>(const SpmmArgs&, cudaStream_t);
 
-template <int VEC, class BT, class AccT, int MINB, int PF>
+template <int VEC, class BT, class AccT, int MINB, int PF, int G = 1>
 int launch_cc_v(const SpmmArgs& a, cudaStream_t st) {
   static int blocks = 0;
-  auto kern = k_spmm_cc<VEC, BT, AccT, MINB, PF>;
+  auto kern = k_spmm_cc<VEC, BT, AccT, MINB, PF, G>;
   if (!blocks) {
     int per_sm = 0;
     RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
@@ -679,6 +691,12 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                      ((uintptr_t)B % (vec * esz)) || ((uintptr_t)C % (vec * 4 < 16 ? vec * 4 : 16))))
     vec >>= 1;
   if (accum == 1 && vec > 4) vec = 4;
+  if (accum == 0 && b_dtype == 0 && (N == 64 || N == 32) && ldb % 4 == 0 && ldc % 4 == 0 && !((uintptr_t)B & 15) &&
+      !((uintptr_t)C & 15)) {
+    // narrow fp32 rows: lane groups take alternate list entries with 16-byte loads
+    if (N == 64) return launch_cc_v<4, float, float, 3, 4, 2>(a, st);
+    return launch_cc_v<4, float, float, 3, 4, 4>(a, st);
+  }
   if (accum == 0) {
     if (b_dtype == 0) return dispatch_vec<float, float>(a, vec, st);
     if (b_dtype == 1) return dispatch_vec<__nv_bfloat16, float>(a, vec, st);

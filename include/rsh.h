@@ -76,6 +76,13 @@ int rsh_residual_gather(const int64_t* row_ptr, const int32_t* col_idx, const fl
                         const int32_t* resid_rows, int64_t n_res, const int64_t* offsets, int32_t* res_col_id,
                         float* res_values, cudaStream_t stream);
 
+/* ---- row permutation: reorder.py:138-151 permute_rows (out row i = source row order[i]);
+ *      order is a device int64 permutation of 0..n_rows-1 (validated by the caller). -------- */
+size_t rsh_permute_workspace(int64_t n_rows);
+int rsh_permute_rows(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
+                     const int64_t* order, int64_t* out_row_ptr, int32_t* out_col_idx, float* out_values, void* ws,
+                     size_t ws_bytes, cudaStream_t stream);
+
 /* ---- persistent-kernel schedule: execute.py:136-168 (_window_groups, value starts) as device
  *      data.  Logical windows are cut into units of chunk_blocks blocks (>= 32; rsh_spmm_cc is
  *      tuned for 32, rsh_spmm_tc for 256) at fixed offsets, so results never depend on the
@@ -107,6 +114,27 @@ int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 const int64_t* res_offset, const int32_t* res_col_id, const float* res_values, int64_t n_res,
                 const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t l1,
                 void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
+
+/* ---- format checks and decode: tile.py:176-267 validate_rstile, tile.py:270-307 decode_rstile.
+ *      rsh_validate writes rsh_report_slots() int64 facts (first offending index per check,
+ *      ranges, popcount sum) that the host turns into the reference's messages; rsh_decode
+ *      rebuilds CSR (row_ptr[n_rows+1], col_idx/values[tc_nnz + res_nnz]) from a valid format,
+ *      dup_out[0] = first duplicate position or -1 (non-canonical result). ------------------ */
+int rsh_report_slots(void);
+size_t rsh_validate_workspace(int64_t n_rows, int64_t n_entries, int64_t n_blocks);
+int rsh_validate(int64_t n_rows, int64_t n_cols, int32_t window_size, const int32_t* row_window_id,
+                 const int64_t* row_window_offset, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
+                 int64_t n_col_id, int64_t n_blocks, int64_t n_values, const int32_t* res_row_id,
+                 const int64_t* res_offset, int64_t n_res, const int32_t* res_col_id, int64_t n_res_col,
+                 int32_t check_bits, int32_t check_cover, int64_t* rep, void* ws, size_t ws_bytes,
+                 cudaStream_t stream);
+size_t rsh_decode_workspace(int64_t n_rows, int64_t nnz, int64_t n_blocks);
+int rsh_decode(int64_t n_rows, int64_t n_cols, const int32_t* row_window_id, const int64_t* row_window_offset,
+               int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id, const float* tc_values,
+               int64_t n_blocks, int64_t tc_nnz, const int32_t* res_row_id, const int64_t* res_offset, int64_t n_res,
+               const int32_t* res_col_id, const float* res_values, int64_t res_nnz, int64_t* out_row_ptr,
+               int32_t* out_col_idx, float* out_values, int64_t* dup_out, void* ws, size_t ws_bytes,
+               cudaStream_t stream);
 
 /* debug: per-CTA role cycle counters of the last rsh_spmm_tc launches run with l1 bit 4 set
  * (host_out: 1024 x 16 uint64), cleared after reading */

@@ -35,6 +35,8 @@ SIGNATURES = {
     "rsh_residual_workspace": (_sz, [_i64]),
     "rsh_residual_offsets": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "rsh_residual_gather": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "rsh_permute_workspace": (_sz, [_i64]),
+    "rsh_permute_rows": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "rsh_schedule_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "rsh_schedule": (ctypes.c_int, [_i64, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]),
     "rsh_partials_bytes": (_sz, [_i64, _i64, _i32]),
@@ -43,6 +45,13 @@ SIGNATURES = {
     "rsh_spmm_tc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
                                    _i32, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
     "rsh_tc_profile": (ctypes.c_int, [_vp]),
+    "rsh_report_slots": (ctypes.c_int, []),
+    "rsh_validate_workspace": (_sz, [_i64, _i64, _i64]),
+    "rsh_validate": (ctypes.c_int, [_i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64,
+                                    _vp, _i64, _i32, _i32, _vp, _vp, _sz, _vp]),
+    "rsh_decode_workspace": (_sz, [_i64, _i64, _i64]),
+    "rsh_decode": (ctypes.c_int, [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp,
+                                  _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "rsh_max_relative_error": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
 }
 

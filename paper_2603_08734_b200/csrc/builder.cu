@@ -588,3 +588,69 @@ int rsh_residual_gather(const int64_t* row_ptr, const int32_t* col_idx, const fl
 }
 
 }  // extern "C"
+
+// ==========================================================================================
+// row permutation (reorder.py:138-151 permute_rows): out row i = source row order[i]
+// ==========================================================================================
+namespace rsh {
+
+__global__ void k_perm_counts(const int64_t* __restrict__ rp, const int64_t* __restrict__ order, int64_t n,
+                              int64_t* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = i < n ? rp[order[i] + 1] - rp[order[i]] : 0;
+}
+
+__global__ void k_perm_copy(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const float* __restrict__ va,
+                            const int64_t* __restrict__ order, int64_t n, const int64_t* __restrict__ out_rp,
+                            int32_t* out_ci, float* out_va) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t s = rp[order[i]], e = rp[order[i] + 1], o = out_rp[i];
+    for (int64_t p = s + lane; p < e; p += 32) {
+      out_ci[o + p - s] = ci[p];
+      out_va[o + p - s] = va[p];
+    }
+  }
+}
+
+}  // namespace rsh
+
+extern "C" {
+
+size_t rsh_permute_workspace(int64_t n_rows) {
+  rsh::Carve cv(nullptr);
+  cv.take<int64_t>(n_rows + 1);
+  size_t a = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, a, (int64_t*)nullptr, (int64_t*)nullptr, (int)(n_rows + 1));
+  cv.take<char>(a);
+  return cv.used + 256;
+}
+
+// reorder.py:138-151.  order: device int64[n_rows], a permutation of 0..n_rows-1 (the caller
+// validates it, as Permutation does, reorder.py:95-107).  Writes out_row_ptr[n_rows+1],
+// out_col_idx[nnz], out_values[nnz].
+int rsh_permute_rows(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
+                     const int64_t* order, int64_t* out_row_ptr, int32_t* out_col_idx, float* out_values, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+  using namespace rsh;
+  if (n_rows < 0) return fail(kInvalid, "rsh_permute_rows: bad n_rows");
+  size_t need = rsh_permute_workspace(n_rows);
+  if (!ws || ws_bytes < need) return fail(kInvalid, "rsh_permute_rows: workspace too small");
+  Carve cv(ws);
+  int64_t* cnt = cv.take<int64_t>(n_rows + 1);
+  size_t cb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(n_rows + 1));
+  void* tmp = cv.take<char>(cb);
+  k_perm_counts<<<grid_1d(n_rows + 1), kThreads, 0, st>>>(row_ptr, order, n_rows, cnt);
+  RSH_LAUNCHED("k_perm_counts");
+  RSH_CUDA(cub::DeviceScan::ExclusiveSum(tmp, cb, cnt, out_row_ptr, (int)(n_rows + 1), st));
+  if (n_rows) {
+    k_perm_copy<<<grid_1d(n_rows * 32), kThreads, 0, st>>>(row_ptr, col_idx, values, order, n_rows, out_row_ptr,
+                                                            out_col_idx, out_values);
+    RSH_LAUNCHED("k_perm_copy");
+  }
+  return kOk;
+}
+
+}  // extern "C"

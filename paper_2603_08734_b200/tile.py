@@ -140,5 +140,154 @@ def build_rstile(a: CsrMatrix, plan: PartitionPlan) -> RsTileMatrix:
     return tile_from_device(build_rstile_device(a, plan))
 
 
+# ---------------------------------------------------------------------------------------------
+# validation and decoding (tile.py:176-307).  The structural facts are computed on device by
+# rsh_validate (csrc/tile_ops.cu); this host side only turns them into the reference's messages,
+# in the reference's order, including its two early returns and its two "only when clean" checks.
+# ---------------------------------------------------------------------------------------------
+
+# report slots, csrc/tile_ops.cu enum Rep
+(_OFF0, _OFF_LAST, _OFF_NONMONO, _COL_MIN, _COL_MAX, _RWID_MIN, _RWID_MAX, _POP_SUM, _POP_OVER,
+ _BIT_BEYOND, _ROFF0, _ROFF_LAST, _ROFF_NONMONO, _RROW_NONINC, _RROW_MIN, _RROW_MAX, _RCOL_MIN,
+ _RCOL_MAX, _RES_IN_WINDOW, _DUP_HEAD, _N_SLOTS) = range(21)
+_NONE = np.iinfo(np.int64).max
+
+
+def _report(t, res_ok: bool, check_bits: bool, check_cover: bool) -> np.ndarray:
+    import torch
+    from ._lib import call, lib
+    from .device import _ptr, _stream, _ws
+    dev = t.device
+    if lib().rsh_report_slots() != _N_SLOTS:
+        raise RuntimeError("librsh.so report layout does not match this package")
+    rep = torch.empty(_N_SLOTS, dtype=torch.int64, device=dev)
+    if res_ok:
+        rr, ro, rc, n_res, n_rc = t.res_row_id, t.res_offset, t.res_col_id, t.n_res, t.res_col_id.numel()
+    else:  # the reference stops before the residual checks; give the kernel an empty residual part
+        ro = torch.zeros(1, dtype=torch.int64, device=dev)
+        rr, rc, n_res, n_rc = None, None, 0, 0
+    nbytes = lib().rsh_validate_workspace(t.n_rows, t.n_entries, t.n_blocks)
+    ws = _ws(nbytes, dev)
+    call("rsh_validate", t.n_rows, t.n_cols, t.window_size, _ptr(t.row_window_id), _ptr(t.row_window_offset),
+         t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id), t.col_id.numel(), t.n_blocks, t.values.numel(),
+         _ptr(rr), _ptr(ro), n_res, _ptr(rc), n_rc, int(check_bits), int(check_cover), _ptr(rep), _ptr(ws),
+         nbytes, _stream())
+    return rep.cpu().numpy()
+
+
+def validate_rstile_device(t) -> list[str]:
+    """tile.py:176-267 for a DeviceTile: every structural invariant, checked on device; an empty
+    list means valid.  Messages and their order are the reference's."""
+    issues: list[str] = []
+    E, nb, R = t.n_entries, t.n_blocks, t.n_res
+    n_values, n_rc = t.values.numel(), t.res_col_id.numel()
+    if not (1 <= t.window_size <= 8):
+        issues.append(f"window_size {t.window_size} outside 1..8")
+    if t.row_window_offset.numel() != E + 1:
+        issues.append("row_window_offset length must be entries + 1")
+        return issues
+    res_ok = t.res_offset.numel() == R + 1
+    r = _report(t, res_ok, False, False)
+
+    def tc_checks(r) -> list[str]:
+        out: list[str] = []
+        if r[_OFF0] != 0:
+            out.append("row_window_offset must start at 0")
+        if r[_OFF_NONMONO] != _NONE:
+            out.append("row_window_offset not monotone")
+        if r[_OFF_LAST] != nb:
+            out.append("row_window_offset end does not equal block count")
+        if t.col_id.numel() != nb * 8:
+            out.append("col_id length must be 8 per block")
+        if t.col_id.numel() and (r[_COL_MIN] < 0 or r[_COL_MAX] >= t.n_cols):
+            out.append("col_id entry out of range")
+        if E:
+            if r[_RWID_MIN] < 0 or r[_RWID_MAX] >= t.n_rows:
+                out.append("row_window_id out of range")
+            if r[_DUP_HEAD] != _NONE:
+                rid = int(t.row_window_id[int(r[_DUP_HEAD])].item())
+                out.append(f"entries sharing row window {rid} are not consecutive segments")
+        if r[_POP_SUM] != n_values:
+            where = int(r[_POP_OVER]) if r[_POP_OVER] != _NONE else nb - 1
+            out.append(f"bitmap popcount sum {int(r[_POP_SUM])} does not match value count "
+                       f"{n_values} (first divergence at block {where})")
+        return out
+
+    def res_checks(r) -> list[str]:
+        out: list[str] = []
+        if r[_ROFF0] != 0:
+            out.append("residual offsets must start at 0")
+        if r[_ROFF_NONMONO] != _NONE:
+            out.append("residual offsets not monotone")
+        if r[_ROFF_LAST] != t.res_values.numel() or n_rc != t.res_values.numel():
+            out.append("residual offsets do not match entry count")
+        if R:
+            if r[_RROW_NONINC] != _NONE:
+                out.append("residual row_id not strictly increasing")
+            if r[_RROW_MIN] < 0 or r[_RROW_MAX] >= t.n_rows:
+                out.append("residual row_id out of range")
+        if n_rc and (r[_RCOL_MIN] < 0 or r[_RCOL_MAX] >= t.n_cols):
+            out.append("residual col_id out of range")
+        return out
+
+    issues += tc_checks(r)
+    rest = res_checks(r) if res_ok else []
+    check_bits = bool(nb) and not issues
+    check_cover = res_ok and bool(R) and bool(E) and not issues and not rest
+    if check_bits or check_cover:  # second pass: the checks that need a clean format
+        r = _report(t, res_ok, check_bits, check_cover)
+    if check_bits and r[_BIT_BEYOND] != _NONE:
+        issues.append(f"block {int(r[_BIT_BEYOND])} has a bit beyond its window's last row")
+    if not res_ok:
+        issues.append("residual offset length must be rows + 1")
+        return issues
+    issues += rest
+    if check_cover and not issues and r[_RES_IN_WINDOW] != _NONE:
+        row = int(t.res_row_id[int(r[_RES_IN_WINDOW])].item())
+        issues.append(f"residual row {row} lies inside a window's row range")
+    return issues
+
+
+def validate_rstile(m: RsTileMatrix) -> list[str]:
+    """tile.py:176-267: check every structural invariant; an empty list means valid."""
+    return validate_rstile_device(tile_to_device(m))
+
+
+def decode_rstile_device(t):
+    """tile.py:270-307 for a DeviceTile -> (DeviceCsr, first duplicate position or -1).  The
+    format must be valid (validate_rstile_device); padding contributes nothing."""
+    import torch
+    from ._lib import call, lib
+    from .device import DeviceCsr, _ptr, _stream, _ws
+    dev = t.device
+    tc_nnz, res_nnz = t.values.numel(), t.res_values.numel()
+    nnz = tc_nnz + res_nnz
+    rp = torch.empty(t.n_rows + 1, dtype=torch.int64, device=dev)
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    va = torch.empty(max(nnz, 1), dtype=torch.float32, device=dev)
+    dup = torch.empty(1, dtype=torch.int64, device=dev)
+    nbytes = lib().rsh_decode_workspace(t.n_rows, nnz, t.n_blocks)
+    ws = _ws(nbytes, dev)
+    call("rsh_decode", t.n_rows, t.n_cols, _ptr(t.row_window_id), _ptr(t.row_window_offset), t.n_entries,
+         _ptr(t.bitmaps), _ptr(t.col_id), _ptr(t.values), t.n_blocks, tc_nnz, _ptr(t.res_row_id),
+         _ptr(t.res_offset), t.n_res, _ptr(t.res_col_id), _ptr(t.res_values), res_nnz, _ptr(rp), _ptr(ci),
+         _ptr(va), _ptr(dup), _ptr(ws), nbytes, _stream())
+    return DeviceCsr(t.n_rows, t.n_cols, rp, ci[:nnz], va[:nnz]), int(dup.item())
+
+
+def decode_rstile(m: RsTileMatrix) -> CsrMatrix:
+    """tile.py:270-307: reconstruct the original CSR exactly (decoded on device)."""
+    issues = validate_rstile(m)
+    if issues:
+        raise FormatError(issues[0])
+    d, _dup = decode_rstile_device(tile_to_device(m))
+    try:  # the reference's canonical-CSR check and its message
+        return CsrMatrix(m.n_rows, m.n_cols, d.row_ptr.cpu().numpy(), d.col_idx.cpu().numpy(),
+                         d.values.cpu().numpy())
+    except ValueError as exc:
+        raise FormatError(f"decoded arrays are not canonical: {exc}") from exc
+
+
 __all__ = ["FormatError", "TcPart", "ResidualPart", "RsTileMatrix", "build_rstile",
-           "build_rstile_device", "tile_from_device", "tile_to_device"]
+           "build_rstile_device", "decode_rstile", "decode_rstile_device", "tile_from_device",
+           "tile_to_device", "validate_rstile", "validate_rstile_device"]

@@ -271,3 +271,18 @@ def test_device_api_out_buffer_and_errors():
     m = build(a)
     with pytest.raises(ValueError):
         P.hybrid_spmm(m, P.DenseMatrix.from_array(rand_b(129, 4, 0)))
+
+
+def test_permute_rows_matches_reference_semantics(small_corpus):
+    """reorder.py:138-151: row i <- source row order[i]; formats built for the same permutation
+    are bit-exact with the oracle's build of the permuted matrix."""
+    for i, a in enumerate(small_corpus[:8]):
+        order = np.random.default_rng(i).permutation(a.n_rows)
+        got = P.permute_rows(a, P.Permutation(order, 0.0))
+        dense = a.to_dense()[order]
+        assert P.csr_equal(got, P.CsrMatrix.from_dense(dense))
+        m = build(got)
+        want = O.build_format(O.Csr.of(got))
+        assert O.tiles_equal(O.Tile.of(m), want) == []
+    with pytest.raises(ValueError):
+        P.Permutation(np.array([0, 0, 1]), 0.0)

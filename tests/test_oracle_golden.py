@@ -121,3 +121,26 @@ def test_config1_routing_matches_survey(name, expect):
     a = O.Csr.of(synth.workload_matrix(name))
     t = O.build_format(a)
     assert (t.row_window_id.size, t.res_row_id.size, t.bitmaps.size) == expect
+
+
+def test_oracle_decode_matches_reference_validate_cases():
+    """The oracle decode reproduces the reference's decode of every valid golden format
+    (tests/golden/validate_cases.*, made by running the reference)."""
+    with open(os.path.join(GOLDEN, "validate_cases.json")) as fh:
+        cases = json.load(fh)
+    arrs = np.load(os.path.join(GOLDEN, "validate_cases.npz"))
+    n_ok = 0
+    for rec in cases:
+        if "csr" not in rec["decode"]:
+            continue
+        k = rec["case"]
+        t = O.Tile(rec["n_rows"], rec["n_cols"],
+                   *(arrs[f"{k}/tc.{f}"] for f in ("row_window_id", "row_window_offset", "bitmaps", "col_id",
+                                                    "values")),
+                   *(arrs[f"{k}/residual.{f}"] for f in ("row_id", "row_nnz_offset", "col_id", "values")),
+                   rec["window_size"])
+        d = O.decode(t)
+        assert digest(np.array([d.n_rows, d.n_cols]), d.row_ptr, d.col_idx.astype(np.int32),
+                      d.values) == rec["decode"]["csr"], k
+        n_ok += 1
+    assert n_ok >= 7

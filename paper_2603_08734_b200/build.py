@@ -6,6 +6,7 @@ only when a source is newer than the library.
 
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -35,7 +36,7 @@ def build(verbose: bool = False) -> str:
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "rsh.h"))
     headers = [h for h in headers if os.path.exists(h)]
-    objs = []
+    objs, jobs = [], []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
@@ -43,12 +44,20 @@ def build(verbose: bool = False) -> str:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
         if _stale(obj, [path] + headers):
-            cmd = [NVCC, *FLAGS, "-I", CSRC, "-I", os.path.join(os.path.dirname(HERE), "include"),
-                   "-c", path, "-o", obj]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            log = os.path.join(objdir, src + ".ptxas.txt")
-            with open(log, "w") as fh:
-                fh.write(r.stdout + r.stderr)
+            jobs.append((src, path, obj))
+
+    def compile_one(job):
+        src, path, obj = job
+        cmd = [NVCC, *FLAGS, "-I", CSRC, "-I", os.path.join(os.path.dirname(HERE), "include"),
+               "-c", path, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        with open(os.path.join(objdir, src + ".ptxas.txt"), "w") as fh:
+            fh.write(r.stdout + r.stderr)
+        return src, r
+
+    # one nvcc per translation unit, in parallel (spmm_cc.cu alone instantiates ~40 kernels)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for src, r in ex.map(compile_one, jobs):
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed on {src}")

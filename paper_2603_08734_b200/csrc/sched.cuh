@@ -13,7 +13,7 @@ constexpr int kChunkCC = 32;    // CUDA-core path: one warp walks a unit seriall
 constexpr int kChunkTC = 256;   // tensor-core path: a unit stays in one TMEM accumulator
 constexpr int kTicketMax = 64;  // windows with more chunks are reduced by the fixup kernels
 constexpr int kFixSeg = 32;     // chunks per first-level fixup segment
-constexpr int kResRows = 8;     // residual rows per unit
+constexpr int kResRows = 16;    // residual rows per unit
 constexpr int kZeroRows = 32;   // uncovered rows per unit
 
 enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
@@ -21,7 +21,7 @@ enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
 // header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
 //         [5]=blocks per window unit (the fixed chunking) [6]=windows reduced by the fixup
 //         kernels (more than kTicketMax chunks) [7]=their first-level fix-up segments
-// counters: uint32 [0]=next unit [1]=warps done
+// counters: uint32 [0]=next unit [1]=warps done [2]=hot-column masks valid
 struct Sched {
   int64_t* header;
   int64_t* unit_cost;  // exclusive prefix of window-unit cost (blocks + 1), [max_units + 1]
@@ -36,6 +36,7 @@ struct Sched {
   uint8_t* uncov_flag;
   int32_t* uncovered;
   int4* units;
+  uint8_t* hot;  // per block: bit j set = col_id slot j names a hot B row (L2 evict_last); valid iff counters[2]
   void* cub;
   size_t cub_bytes;
   int64_t max_units;
@@ -67,6 +68,7 @@ inline size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_
   s->uncovered = cv.take<int32_t>(n_rows + 1);
   s->max_units = E + n_blocks / kChunkMin + 1 + (n_res + kResRows - 1) / kResRows + (n_rows + kZeroRows - 1) / kZeroRows + 4;
   s->units = cv.take<int4>(s->max_units);
+  s->hot = cv.take<uint8_t>(n_blocks + 1);
   s->unit_cost = cv.take<int64_t>(s->max_units + 1);
   s->unit_cost_raw = cv.take<int64_t>(s->max_units + 1);
   size_t a = 0, b = 0;
@@ -149,6 +151,8 @@ __device__ __forceinline__ unsigned long long ldg_hint64(const void* p, uint64_t
   asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(u) : "l"(p), "l"(pol));
   return u;
 }
+
+__device__ __forceinline__ int4 make_int4_u(uint4 u) { return make_int4((int)u.x, (int)u.y, (int)u.z, (int)u.w); }
 
 // load_vec with an L2 policy (16-byte multiples; other widths fall back to load_vec)
 template <int VEC, class BT>

@@ -49,14 +49,15 @@ __device__ __forceinline__ int64_t block_reduce(int64_t v, Op op, int64_t* s_red
   if (l == 0) s_red[w] = v;
   __syncthreads();
   if (w == 0) {
-    v = l < (int)(blockDim.x >> 5) ? s_red[l] : s_red[0];
+    // lanes past the last warp repeat warp 0's value: harmless for min / max, wrong for a sum
+    v = l < (int)(blockDim.x >> 5) ? s_red[l] : (Op::kIdempotent ? s_red[0] : 0);
     for (int o = 16; o; o >>= 1) v = op(v, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)v, o));
   }
   return v;  // valid in thread 0
 }
-struct Min { __device__ int64_t operator()(int64_t a, int64_t b) const { return a < b ? a : b; } };
-struct Max { __device__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; } };
-struct Sum { __device__ int64_t operator()(int64_t a, int64_t b) const { return a + b; } };
+struct Min { static constexpr bool kIdempotent = true; __device__ int64_t operator()(int64_t a, int64_t b) const { return a < b ? a : b; } };
+struct Max { static constexpr bool kIdempotent = true; __device__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; } };
+struct Sum { static constexpr bool kIdempotent = false; __device__ int64_t operator()(int64_t a, int64_t b) const { return a + b; } };
 
 __device__ __forceinline__ void amin_s(int64_t* p, int64_t v) { atomicMin((long long*)p, (long long)v); }
 __device__ __forceinline__ void amax_s(int64_t* p, int64_t v) { atomicMax((long long*)p, (long long)v); }

@@ -39,9 +39,15 @@ def summarise(path: str) -> list[dict]:
             if k in hdr:
                 i = hdr.index(k)
                 d[k] = f"{vals[i]} {units[i]}".strip()
-        # any tensor-pipe metric present
+        # any tensor-pipe metric, every warp-stall reason, the global-load L1 sector counts
         for i, h in enumerate(hdr):
-            if "pipe_tensor" in h and "pct" in h and h not in d:
+            want = ("pipe_tensor" in h and "pct" in h) or (
+                h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")) or (
+                h.startswith("l1tex__t_sectors_pipe_lsu_mem_global_op_ld") and h.endswith(".sum")) or (
+                h.startswith("l1tex__t_requests_pipe_lsu_mem_global_op_ld") and h.endswith(".sum")) or (
+                h in ("sm__warps_active.avg.per_cycle_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                      "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__t_bytes.sum"))
+            if want and h not in d:
                 d[h] = f"{vals[i]} {units[i]}".strip()
         res.append(d)
     return res

@@ -218,7 +218,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--math", default="auto", choices=["auto", "fp32", "tf32"])
+    ap.add_argument("--math", default="auto", choices=["auto", "fp32", "tf32", "tc"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -275,7 +275,7 @@ def run_single(args):
     # arithmetic path: fp32 B -> exact FP32 (CUDA cores) or TF32 (tensor cores); bf16 B -> tensor
     # cores when the shape allows.  "auto" times both for a few launches and keeps the faster.
     from paper_2603_08734_b200.device import resolve_math, tc_eligible
-    candidates = ["fp32", "tf32"] if (w.dtype == "f32" and tc_eligible(tile, bt)) else ["auto"]
+    candidates = (["fp32", "tf32"] if w.dtype == "f32" else ["auto", "tc"]) if tc_eligible(tile, bt) else ["auto"]
     if args.math != "auto":
         candidates = [args.math]
     path_ms = {}

@@ -95,18 +95,6 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
                  int64_t* header_out, cudaStream_t stream);
 size_t rsh_partials_bytes(int64_t partial_slots, int64_t n_features, int32_t accum);
 
-/* ---- L2 residency plan for B (no reference counterpart: a B200 cache policy, not a format
- *      change).  The CUDA-core window path gathers one B row per nonzero; rows of the
- *      highest-degree columns that fit budget_bytes are loaded L2::evict_last, the rest
- *      L2::evict_first.  Fills the per-block hot masks inside an rsh_schedule buffer; results
- *      of rsh_spmm_cc are bit-identical with or without it.  ws >= rsh_hot_columns_bytes(n_cols).
- *      stats_out (device int64[3], may be NULL) = [degree threshold, hot rows, hot gathers]. */
-size_t rsh_hot_columns_bytes(int64_t n_cols);
-int rsh_hot_columns(int64_t n_rows, int64_t n_cols, int64_t n_entries, const uint64_t* bitmaps,
-                    const int32_t* col_id, int64_t n_blocks, int64_t n_res, const int32_t* res_col_id,
-                    int64_t res_nnz, int64_t row_bytes, int64_t budget_bytes, void* sched, size_t sched_bytes,
-                    void* ws, size_t ws_bytes, int64_t* stats_out, cudaStream_t stream);
-
 /* ---- hybrid SpMM: execute.py:155-218 hybrid_spmm.  C[n_rows x N] (row stride ldc) is
  *      fully written: window rows assigned, residual rows assigned, all other rows zero.
  *      B[n_cols x N] row stride ldb; b_dtype 0 f32, 1 bf16, 2 f16; accum 0 f32, 1 f64.

@@ -40,9 +40,6 @@ SIGNATURES = {
     "rsh_schedule_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "rsh_schedule": (ctypes.c_int, [_i64, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]),
     "rsh_partials_bytes": (_sz, [_i64, _i64, _i32]),
-    "rsh_hot_columns_bytes": (_sz, [_i64]),
-    "rsh_hot_columns": (ctypes.c_int, [_i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _sz,
-                                       _vp, _sz, _vp, _vp]),
     "rsh_spmm_cc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
                                    _i32, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
     "rsh_spmm_tc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,

@@ -21,7 +21,7 @@ enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
 // header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
 //         [5]=blocks per window unit (the fixed chunking) [6]=windows reduced by the fixup
 //         kernels (more than kTicketMax chunks) [7]=their first-level fix-up segments
-// counters: uint32 [0]=next unit [1]=warps done [2]=hot-column masks valid
+// counters: uint32 [0]=next unit [1]=warps done
 struct Sched {
   int64_t* header;
   int64_t* unit_cost;  // exclusive prefix of window-unit cost (blocks + 1), [max_units + 1]
@@ -36,7 +36,6 @@ struct Sched {
   uint8_t* uncov_flag;
   int32_t* uncovered;
   int4* units;
-  uint8_t* hot;  // per block: bit j set = col_id slot j names a hot B row (L2 evict_last); valid iff counters[2]
   void* cub;
   size_t cub_bytes;
   int64_t max_units;
@@ -68,7 +67,6 @@ inline size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_
   s->uncovered = cv.take<int32_t>(n_rows + 1);
   s->max_units = E + n_blocks / kChunkMin + 1 + (n_res + kResRows - 1) / kResRows + (n_rows + kZeroRows - 1) / kZeroRows + 4;
   s->units = cv.take<int4>(s->max_units);
-  s->hot = cv.take<uint8_t>(n_blocks + 1);
   s->unit_cost = cv.take<int64_t>(s->max_units + 1);
   s->unit_cost_raw = cv.take<int64_t>(s->max_units + 1);
   size_t a = 0, b = 0;

@@ -106,7 +106,6 @@ __global__ void k_finish_header(Sched s, int64_t E, int64_t n_res, int32_t chunk
   s.header[5] = chunk;
   s.counters[0] = 0;
   s.counters[1] = 0;
-  s.counters[2] = 0;  // hot-column masks not computed (rsh_hot_columns sets it)
 }
 
 __global__ void k_tail_units(Sched s, int64_t n_res) {
@@ -122,73 +121,6 @@ __global__ void k_tail_units(Sched s, int64_t n_res) {
       s.units[uw + i] = make_int4(kUnitZero, (int32_t)lo, (int32_t)hi, 0);
     }
   }
-}
-
-// ------------------------------------------------------------------------------------------
-// hot B rows: an L2 residency plan.  The window path gathers one B row per nonzero, so B row c is
-// read deg(c) times (its column's nonzero count).  The rows of the highest-degree columns whose
-// bytes fit the budget are loaded with L2::evict_last, all others with L2::evict_first, so the
-// rarely reused rows stop displacing the heavily reused ones (a frequency-aware replacement
-// policy the LRU-like L2 cannot infer on its own).  Preprocessing, built once per format.
-// ------------------------------------------------------------------------------------------
-
-constexpr int kDegBins = 4096;  // degree histogram bins (the last one holds every larger degree)
-
-__global__ void k_col_degree(const unsigned long long* __restrict__ bm, const int32_t* __restrict__ col, int64_t nb,
-                             const int32_t* __restrict__ res_col, int64_t res_nnz, int32_t* deg) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = tid; i < nb * 8; i += stride) {
-    const unsigned long long m = bm[i >> 3];
-    const int j = (int)(i & 7);
-    const int n = __popcll(m & (0x0101010101010101ull << j));  // rows using slot j
-    if (n) atomicAdd(deg + col[i], n);
-  }
-  for (int64_t p = tid; p < res_nnz; p += stride) atomicAdd(deg + res_col[p], 1);
-}
-
-__global__ void k_deg_hist(const int32_t* __restrict__ deg, int64_t n_cols, int32_t* hist) {
-  __shared__ int32_t h[kDegBins];
-  for (int i = threadIdx.x; i < kDegBins; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cols; c += (int64_t)gridDim.x * blockDim.x) {
-    const int d = deg[c];
-    if (d > 0) atomicAdd(h + (d < kDegBins - 1 ? d : kDegBins - 1), 1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kDegBins; i += blockDim.x)
-    if (h[i]) atomicAdd(hist + i, h[i]);
-}
-
-// smallest degree threshold t whose rows (every column with degree >= t) fit the budget; whole
-// histogram bins only, so equal-degree columns are treated alike.  stats: [t, hot rows, hot gathers]
-__global__ void k_deg_threshold(const int32_t* __restrict__ hist, int64_t row_bytes, int64_t budget, int64_t* stats) {
-  int64_t rows = 0, gathers = 0;
-  int t = kDegBins;  // nothing hot
-  for (int d = kDegBins - 1; d >= 1; --d) {
-    if (d == kDegBins - 1) {  // open-ended bin: cannot be split either
-      if ((rows + hist[d]) * row_bytes > budget) break;
-    } else if ((rows + hist[d]) * row_bytes > budget) {
-      break;
-    }
-    rows += hist[d];
-    gathers += (int64_t)hist[d] * d;
-    t = d;
-  }
-  stats[0] = t;
-  stats[1] = rows;
-  stats[2] = gathers;  // lower bound for the open-ended bin
-}
-
-__global__ void k_hot_masks(const int32_t* __restrict__ col, int64_t nb, const int32_t* __restrict__ deg,
-                            const int64_t* __restrict__ stats, Sched s) {
-  const int64_t t = stats[0];
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) m |= (uint32_t)(deg[col[b * 8 + j]] >= t) << j;
-    s.hot[b] = (uint8_t)m;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) s.counters[2] = 1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -610,17 +542,19 @@ template int launch_fixup<float>(const SpmmArgs&, cudaStream_t);
 // ------------------------------------------------------------------------------------------
 // the streaming CUDA-core kernel (fp32 accumulation): one warp per work unit, the unit's
 // nonzeros listed once in row-major order and then gathered as ONE flat stream with kDepth B-row
-// loads always in flight -- row boundaries are crossed without draining the pipeline, so a
-// warp keeps kDepth x 32 x VEC x 4 bytes outstanding for the whole unit.
+// loads always in flight -- row boundaries are crossed without draining the pipeline.
+//
+// Why shared memory is kept tiny: the gathers are L1-allocating LDG.128s, and an SM can only
+// have as many bytes in flight as its L1 can hold lines for (L1 = 228 KB minus shared memory).
+// The list is 8 bytes per nonzero (kCap entries per warp) and nothing else is staged.
 //
 // Per unit:
-//   1. metadata: window unit -- lane l owns block b0 + l (bitmap, value start); two packed warp
-//      scans of the per-row popcounts give every nonzero its row-major list position.  Residual
-//      unit -- its entries are already contiguous (res_col / res_val), row ends from res_off.
-//   2. list fill: (col, value) pairs copied global -> shared with 4-byte cp.async (no register
-//      round trip, all copies in flight at once), one wait.  Units longer than kCap entries are
-//      streamed in pieces of kCap list positions; the row accumulator carries across pieces.
-//   3. stream: entry e's B row is requested kDepth entries before its FMA; a row's sum is stored
+//   1. window unit: lane l owns block b0 + l; two packed warp scans of the per-row popcounts give
+//      every nonzero its row-major list position, and each lane copies its (col, value) pairs
+//      into the list with 4-byte cp.async (no register round trip, all copies in flight at
+//      once).  Residual unit: its entries are already contiguous (res_col / res_val).  Units
+//      longer than kCap entries are listed and streamed in pieces; the row sum carries over.
+//   2. stream: entry e's B row is requested kDepth entries before its FMA; a row's sum is stored
 //      when the stream crosses the row's end (rows without nonzeros store zeros, as the reference
 //      assigns every window row, execute.py:181-182).
 // The per-row accumulation order -- blocks in order, columns ascending inside a block -- is the
@@ -628,30 +562,26 @@ template int launch_fixup<float>(const SpmmArgs&, cudaStream_t);
 // k_spmm_cc and independent of the schedule.
 // ------------------------------------------------------------------------------------------
 
-constexpr int kCap = 384;      // list entries per warp piece
 constexpr int kMaxRows = 16;   // rows per unit (8 window rows; kResRows residual rows)
 static_assert(kResRows <= kMaxRows, "residual unit larger than the stream row table");
 
+struct UnitDesc {
+  long long s0;      // residual unit: first entry
+  long long rid;     // window unit: first row
+  int window, to_part, total, nrows, g, slot, avail, b0, b1;
+  uint32_t next;     // the unit claimed for after this one
+};
+
+template <int kCap>
 struct StreamSmem {
   int2 list[kCap];
   int rend[kMaxRows + 1];          // row-major list end of each unit row
   long long rowoff[kMaxRows];      // element offset of each unit row in C (or the partials)
-  int4 lcol[32][2];                // window unit: lane's block col_id slots
-  int lhot[32];                    // window unit: lane's block hot-row mask
-  unsigned long long lbm[32];      // window unit: lane's block bitmap
-  unsigned long long loff[2][32];  // window unit: lane's exclusive per-row offsets (4 x 16 bits)
-  int lvs[32];                     // window unit: lane's first value
-  struct {
-    long long s0;                  // residual unit: first entry
-    long long rid;                 // window unit: first row
-    int window, to_part, total, nrows, g, slot, avail;
-    uint32_t next;                 // the unit claimed for after this one
-  } u;
+  UnitDesc u;
 };
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(g) : "memory");
+__device__ __forceinline__ void cp_async4_s(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -662,17 +592,21 @@ struct RawVec {
   uint32_t w[kWords];
 };
 
-template <int VEC, class BT>
+template <int VEC, class BT, bool kNoL1>
 __device__ __forceinline__ void raw_load(const BT* p, RawVec<VEC, BT>& r, uint64_t pol) {
   constexpr int bytes = VEC * (int)sizeof(BT);
   if constexpr (bytes % 16 == 0) {
 #pragma unroll
     for (int q = 0; q < bytes / 16; ++q) {
-      const uint4 u = ldg_hint(reinterpret_cast<const uint4*>(p) + q, pol);
-      r.w[4 * q] = u.x;
-      r.w[4 * q + 1] = u.y;
-      r.w[4 * q + 2] = u.z;
-      r.w[4 * q + 3] = u.w;
+      const uint4* a = reinterpret_cast<const uint4*>(p) + q;
+      if constexpr (kNoL1)
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=r"(r.w[4 * q]), "=r"(r.w[4 * q + 1]), "=r"(r.w[4 * q + 2]), "=r"(r.w[4 * q + 3])
+            : "l"(a), "l"(pol));
+      else
+        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=r"(r.w[4 * q]), "=r"(r.w[4 * q + 1]), "=r"(r.w[4 * q + 2]), "=r"(r.w[4 * q + 3])
+            : "l"(a), "l"(pol));
     }
   } else if constexpr (bytes == 8) {
     const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
@@ -692,61 +626,83 @@ __device__ __forceinline__ void raw_fma(const RawVec<VEC, BT>& r, float v, float
   for (int t = 0; t < VEC; ++t) acc[t] = fmaf(v, to_f<BT>(e[t]), acc[t]);
 }
 
-// B-row slice load with the L2 policy picked per entry (hot rows evict_last, cold evict_first):
-// two predicated loads, one of which issues -- no branch, and both policies stay uniform.
-template <int VEC, class BT>
-__device__ __forceinline__ void raw_load_sel(const BT* p, RawVec<VEC, BT>& r, int hot, uint64_t pol_hot,
-                                             uint64_t pol_cold) {
-  constexpr int bytes = VEC * (int)sizeof(BT);
-  if constexpr (bytes % 16 == 0) {
+// List positions [P0, P0 + kCap) of a window unit.  Every lane re-derives its block's row
+// offsets (loads hit L1 after the first piece); on the first piece the unit's row table is
+// written too.
+template <int kCap>
+__device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>& sm, int P0, uint64_t pol_a) {
+  const int lane = threadIdx.x & 31;
+  const int32_t blk = sm.u.b0 + lane;
+  const bool mine = blk < sm.u.b1;
+  const unsigned long long bm = mine ? ldg_hint64(a.bitmaps + blk, pol_a) : 0ull;
+  const int32_t vs = mine ? __ldg(a.s.vstart + blk) : 0;
+  unsigned long long p0 = 0, p1 = 0;  // this lane's per-row counts, 4 rows x 16 bits per word
 #pragma unroll
-    for (int q = 0; q < bytes / 16; ++q) {
-      asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
-          "@p ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %6;\n\t"
-          "@!p ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %7;\n\t}"
-          : "=r"(r.w[4 * q]), "=r"(r.w[4 * q + 1]), "=r"(r.w[4 * q + 2]), "=r"(r.w[4 * q + 3])
-          : "l"(reinterpret_cast<const uint4*>(p) + q), "r"(hot), "l"(pol_hot), "l"(pol_cold));
-    }
-  } else {
-    raw_load<VEC, BT>(p, r, pol_hot);
+  for (int i = 0; i < 4; ++i) {
+    p0 |= (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
+    p1 |= (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
   }
+  unsigned long long q0 = p0, q1 = p1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t0 = __shfl_up_sync(0xffffffffu, q0, o);
+    const unsigned long long t1 = __shfl_up_sync(0xffffffffu, q1, o);
+    if (lane >= o) {
+      q0 += t0;
+      q1 += t1;
+    }
+  }
+  const unsigned long long tot0 = __shfl_sync(0xffffffffu, q0, 31), tot1 = __shfl_sync(0xffffffffu, q1, 31);
+  const unsigned long long rp0 = tot0 * 0x0001000100010001ull;  // inclusive prefix of the row totals
+  const unsigned long long rp1 = tot1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
+  if (P0 == 0) {
+    if (lane < 8) {
+      sm.rend[lane] = (int)(((lane < 4 ? rp0 : rp1) >> (16 * (lane & 3))) & 0xffffull);
+      const int64_t rid = sm.u.rid;
+      sm.rowoff[lane] = sm.u.slot < 0 ? (rid + lane) * a.ldc : ((int64_t)sm.u.slot * 8 + lane) * a.N;
+    }
+    if (lane == 0) sm.u.total = (int)(rp1 >> 48);
+  }
+  // F(i) = list start of this lane's row-i segment minus the lane's nonzeros before row i, so a
+  // nonzero of rank r (its value index within the block) lands at F(row) + r.  Packed 4 x 16 bit.
+  const unsigned long long ex0 = q0 - p0, ex1 = q1 - p1;  // exclusive lane prefixes per row
+  const unsigned long long beg0 = (rp0 << 16), beg1 = (rp1 << 16) | (rp0 >> 48);  // row starts
+  const unsigned long long below0 = (p0 * 0x0001000100010001ull) << 16;          // nnz of rows < i
+  const unsigned long long below1 = ((p1 * 0x0001000100010001ull) << 16) + ((p0 * 0x0001000100010001ull) >> 48) * 0x0001000100010001ull;
+  // fields stay non-negative: below(i) <= beg(i) + ex(i) always (a lane's own rows < i are part of the list before row i)
+  const unsigned long long F0 = beg0 + ex0 - below0, F1 = beg1 + ex1 - below1;
+  const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(sm.list);
+  const int32_t* cbase = a.col_id + (int64_t)blk * 8;
+  const float* vbase = a.tc_values + vs;
+  const int P1 = P0 + kCap;
+  unsigned long long rem = bm;
+  int r = 0;
+  while (rem) {
+    const int bit = __ffsll((long long)rem) - 1;
+    rem &= rem - 1;
+    const int i = bit >> 3;
+    const int pos = (int)((((i < 4 ? F0 : F1) >> (16 * (i & 3))) & 0xffffull)) + r;
+    if (pos >= P0 && pos < P1) {
+      const uint32_t d = list_s + (uint32_t)(pos - P0) * 8u;
+      cp_async4_s(d, cbase + (bit & 7));
+      cp_async4_s(d + 4, vbase + r);
+    }
+    ++r;
+  }
+  cp_async_wait_all();
+  __syncwarp();
 }
 
-// Fill list positions [P0, P0 + kCap) of the warp's current unit (descriptor in sm.u).
-__device__ __forceinline__ void stream_fill(const SpmmArgs& a, StreamSmem& sm, int P0) {
+template <int kCap>
+__device__ __forceinline__ void residual_fill(const SpmmArgs& a, StreamSmem<kCap>& sm, int P0) {
   const int lane = threadIdx.x & 31;
-  const int P1 = P0 + kCap;
-  if (sm.u.window) {
-    const unsigned long long bm = sm.lbm[lane];
-    const unsigned long long o0 = sm.loff[0][lane], o1 = sm.loff[1][lane];
-    const int32_t vs = sm.lvs[lane];
-    const int* lcol = reinterpret_cast<const int*>(sm.lcol[lane]);
-    const int hotm = sm.lhot[lane];
-    unsigned long long rem = bm;
-    int vrank = 0;
-    while (rem) {
-      const int bit = __ffsll((long long)rem) - 1;
-      rem &= rem - 1;
-      const int i = bit >> 3, j = bit & 7;
-      const int row_beg = i ? sm.rend[i - 1] : 0;
-      const int lane_off = (int)(((i < 4 ? o0 : o1) >> (16 * (i & 3))) & 0xffffull);
-      const uint32_t byte = uint32_t(bm >> (8 * i)) & 0xffu;
-      const int pos = row_beg + lane_off + __popc(byte & ((1u << j) - 1u));
-      if (pos >= P0 && pos < P1) {
-        int2* dst = sm.list + (pos - P0);
-        dst->x = lcol[j] | (((hotm >> j) & 1) << 31);  // bit 31: hot B row (L2 evict_last)
-        cp_async4(&dst->y, a.tc_values + vs + vrank);
-      }
-      ++vrank;
-    }
-  } else {
-    const int64_t s0 = sm.u.s0;
-    const int total = sm.u.total;
-    const int n = total - P0 < kCap ? total - P0 : kCap;
-    for (int p = lane; p < n; p += 32) {
-      sm.list[p].x = __ldg(a.res_col + s0 + P0 + p) | (1 << 31);
-      cp_async4(&sm.list[p].y, a.res_val + s0 + P0 + p);
-    }
+  const int64_t s0 = sm.u.s0 + P0;
+  const int total = sm.u.total;
+  const int n = total - P0 < kCap ? total - P0 : kCap;
+  const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(sm.list);
+  for (int p = lane; p < n; p += 32) {
+    cp_async4_s(list_s + 8u * p, a.res_col + s0 + p);
+    cp_async4_s(list_s + 8u * p + 4, a.res_val + s0 + p);
   }
   cp_async_wait_all();
   __syncwarp();
@@ -754,10 +710,15 @@ __device__ __forceinline__ void stream_fill(const SpmmArgs& a, StreamSmem& sm, i
 
 // Stream the unit's row-major list (pieces of kCap positions) with kDepth B-row loads in flight.
 // Bf = B + this lane's first feature; out = C (or the partials) + the same feature offset.
-template <int VEC, class BT, int kDepth, bool kFull>
-__device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem& sm, const BT* __restrict__ Bf, bool active,
-                                            int fc, float* __restrict__ out, uint64_t pol_hot, uint64_t pol_cold) {
-  const int64_t ldb = a.ldb;
+// Entries are consumed in groups of kDepth: a group that stays inside the current row (the
+// common case) runs without any per-entry row test; only groups that reach a row end take the
+// per-entry path that stores finished rows.
+template <int VEC, class BT, int kDepth, bool kFull, bool kNoL1, int kCap>
+__device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem<kCap>& sm, const BT* __restrict__ Bf,
+                                            bool active, int fc, float* __restrict__ out, uint64_t pol_b,
+                                            uint64_t pol_a) {
+  const char* const Bc = reinterpret_cast<const char*>(Bf);
+  const uint32_t rstride = (uint32_t)(a.ldb * (int64_t)sizeof(BT));  // bytes per B row (< 4 GiB, checked on the host)
   const int total = sm.u.total;
   const bool single = total <= kCap;
   float acc[VEC];
@@ -766,58 +727,58 @@ __device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem& sm, c
   int cur = 0;
   int nxt_end = sm.rend[0];
   auto flush = [&]() {
-    if (kFull || active) {
-      float* dst = out + sm.rowoff[cur];
-      if (sm.u.to_part) {
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) __stcg(dst + t, acc[t]);
-      } else {
-        store_c<VEC, float>(dst, acc);
-      }
-    }
+    if (kFull || active) store_c<VEC, float>(out + sm.rowoff[cur], acc);
 #pragma unroll
     for (int t = 0; t < VEC; ++t) acc[t] = 0.f;
     ++cur;
     nxt_end = sm.rend[cur];
   };
+  auto issue = [&](int idx, RawVec<VEC, BT>& r, float& v) {
+    const int2 cv = sm.list[idx];
+    v = __int_as_float(cv.y);
+    if (kFull || active)
+      raw_load<VEC, BT, kNoL1>(reinterpret_cast<const BT*>(Bc + (uint64_t)(uint32_t)cv.x * rstride), r, pol_b);
+  };
   for (int P0 = 0; P0 < total; P0 += kCap) {
-    if (!single || fc == 0) {
-      if (!single) __syncwarp();  // the previous piece's list reads are done
-      stream_fill(a, sm, P0);
+    if (P0 > 0 || (fc > 0 && !single)) {
+      __syncwarp();  // the previous piece's list reads are done
+      if (sm.u.window) window_fill<kCap>(a, sm, P0, pol_a);
+      else residual_fill<kCap>(a, sm, P0);
     }
     const int len = total - P0 < kCap ? total - P0 : kCap;
     RawVec<VEC, BT> rb[kDepth];
     float vv[kDepth];
 #pragma unroll
-    for (int p = 0; p < kDepth; ++p) {
-      if (p < len) {
-        const int2 cv = sm.list[p];
-        vv[p] = __int_as_float(cv.y);
-        if (kFull || active)
-          raw_load_sel<VEC, BT>(Bf + (int64_t)(cv.x & 0x7fffffff) * ldb, rb[p], cv.x < 0, pol_hot, pol_cold);
-      }
-    }
+    for (int p = 0; p < kDepth; ++p)
+      if (p < len) issue(p, rb[p], vv[p]);
     int base = 0;
-    for (; base + kDepth <= len; base += kDepth) {
+    // steady state: every refill index base + kDepth + p is inside the piece
+    for (; base + 2 * kDepth <= len; base += kDepth) {
+      if (P0 + base + kDepth - 1 < nxt_end) {
 #pragma unroll
-      for (int p = 0; p < kDepth; ++p) {
-        const int e = base + p;
-        while (P0 + e >= nxt_end) flush();
-        if (kFull || active) raw_fma<VEC, BT>(rb[p], vv[p], acc);
-        if (e + kDepth < len) {
-          const int2 cv = sm.list[e + kDepth];
-          vv[p] = __int_as_float(cv.y);
-          if (kFull || active)
-            raw_load_sel<VEC, BT>(Bf + (int64_t)(cv.x & 0x7fffffff) * ldb, rb[p], cv.x < 0, pol_hot, pol_cold);
+        for (int p = 0; p < kDepth; ++p) {
+          if (kFull || active) raw_fma<VEC, BT>(rb[p], vv[p], acc);
+          issue(base + kDepth + p, rb[p], vv[p]);
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < kDepth; ++p) {
+          while (P0 + base + p >= nxt_end) flush();
+          if (kFull || active) raw_fma<VEC, BT>(rb[p], vv[p], acc);
+          issue(base + kDepth + p, rb[p], vv[p]);
         }
       }
     }
+    // drain: the last one or two groups
+    for (; base < len; base += kDepth) {
 #pragma unroll
-    for (int p = 0; p < kDepth; ++p) {
-      const int e = base + p;
-      if (e < len) {
-        while (P0 + e >= nxt_end) flush();
-        if (kFull || active) raw_fma<VEC, BT>(rb[p], vv[p], acc);
+      for (int p = 0; p < kDepth; ++p) {
+        const int e = base + p;
+        if (e < len) {
+          while (P0 + e >= nxt_end) flush();
+          if (kFull || active) raw_fma<VEC, BT>(rb[p], vv[p], acc);
+          if (e + kDepth < len) issue(e + kDepth, rb[p], vv[p]);
+        }
       }
     }
   }
@@ -825,17 +786,15 @@ __device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem& sm, c
   while (cur < nrows) flush();
 }
 
-template <int VEC, class BT, int kDepth, int MINB, bool kFull>
+template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
-  __shared__ StreamSmem smem_all[kThreads / 32];
-  StreamSmem& sm = smem_all[threadIdx.x >> 5];
+  __shared__ StreamSmem<kCap> smem_all[kThreads / 32];
+  StreamSmem<kCap>& sm = smem_all[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t total_units = a.s.header[2];
   const int n_fc = (a.N + 32 * VEC - 1) / (32 * VEC);
   const BT* B = reinterpret_cast<const BT*>(a.B);
-  const bool hints = !(a.flags & 4);
-  const uint64_t pol_b = hints ? policy_evict_last() : 0, pol_a = hints ? policy_evict_first() : 0;
-  const bool hot_on = hints && !(a.flags & 128) && a.s.counters[2] != 0;  // per-column L2 residency plan
+  const uint64_t pol_b = policy_evict_last(), pol_a = policy_evict_first();
 
   uint32_t u = 0;
   if (lane == 0) u = atomicAdd(a.s.counters, 1u);
@@ -849,57 +808,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
       zero_rows<VEC>(a, un.y, un.z);
     } else {
       if (type == kUnitWindow) {
-        const int32_t g = un.y, k = un.x >> 2;
-        const int64_t rid = a.s.grp_rid[g];
-        const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
-        const int32_t slot = a.s.grp_slot[g];
-        const int32_t blk = un.z + lane;
-        const bool mine = blk < un.w;
-        const unsigned long long bm =
-            mine ? (hints ? ldg_hint64(a.bitmaps + blk, pol_a) : __ldg(a.bitmaps + blk)) : 0ull;
-        sm.lvs[lane] = mine ? __ldg(a.s.vstart + blk) : 0;
-        if (mine) {
-          const int4* cp = reinterpret_cast<const int4*>(a.col_id + (int64_t)blk * 8);
-          sm.lcol[lane][0] = hints ? make_int4_u(ldg_hint(cp, pol_a)) : __ldg(cp);
-          sm.lcol[lane][1] = hints ? make_int4_u(ldg_hint(cp + 1, pol_a)) : __ldg(cp + 1);
-          sm.lhot[lane] = hot_on ? (int)__ldg(a.s.hot + blk) : 0xff;
-        }
-        unsigned long long p0 = 0, p1 = 0;  // this lane's per-row counts, 4 rows x 16 bits per word
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          p0 |= (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
-          p1 |= (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
-        }
-        unsigned long long q0 = p0, q1 = p1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned long long t0 = __shfl_up_sync(0xffffffffu, q0, o);
-          const unsigned long long t1 = __shfl_up_sync(0xffffffffu, q1, o);
-          if (lane >= o) {
-            q0 += t0;
-            q1 += t1;
-          }
-        }
-        const unsigned long long tot0 = __shfl_sync(0xffffffffu, q0, 31), tot1 = __shfl_sync(0xffffffffu, q1, 31);
-        const unsigned long long rp0 = tot0 * 0x0001000100010001ull;  // inclusive prefix of the row totals
-        const unsigned long long rp1 = tot1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
-        sm.lbm[lane] = bm;
-        sm.loff[0][lane] = q0 - p0;  // exclusive lane prefixes per row
-        sm.loff[1][lane] = q1 - p1;
-        if (lane < 8) {
-          sm.rend[lane] = (int)(((lane < 4 ? rp0 : rp1) >> (16 * (lane & 3))) & 0xffffull);
-          sm.rowoff[lane] = slot < 0 ? (rid + lane) * a.ldc : ((int64_t)(slot + k) * 8 + lane) * a.N;
-        }
         if (lane == 0) {
+          const int32_t g = un.y;
+          const int64_t rid = a.s.grp_rid[g];
+          const int32_t slot = a.s.grp_slot[g];
           sm.u.window = 1;
           sm.u.to_part = slot >= 0;
-          sm.u.total = (int)(rp1 >> 48);
-          sm.u.nrows = slot < 0 ? (int)avail : 8;
           sm.u.g = g;
-          sm.u.slot = slot;
+          // chunk k of a multi-chunk window writes partial slot (slot + k)
+          sm.u.slot = slot < 0 ? -1 : slot + (un.x >> 2);
           sm.u.rid = rid;
+          const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
           sm.u.avail = (int)avail;
+          sm.u.nrows = slot < 0 ? (int)avail : 8;
+          sm.u.b0 = un.z;
+          sm.u.b1 = un.w;
         }
+        __syncwarp();
+        window_fill<kCap>(a, sm, 0, pol_a);
       } else {
         const int32_t i0 = un.y, i1 = un.z;
         const int nr = i1 - i0;
@@ -916,14 +842,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
           sm.u.s0 = s0;
           sm.u.slot = -1;
         }
+        __syncwarp();
+        residual_fill<kCap>(a, sm, 0);
       }
-      __syncwarp();
       float* const out_base = sm.u.to_part ? reinterpret_cast<float*>(a.partials) : a.C;
       for (int fc = 0; fc < n_fc; ++fc) {
         const int f0 = fc * 32 * VEC + lane * VEC;
-        stream_rows<VEC, BT, kDepth, kFull>(a, sm, B + f0, f0 < a.N, fc, out_base + f0, pol_b, pol_a);
+        stream_rows<VEC, BT, kDepth, kFull, kNoL1, kCap>(a, sm, B + f0, f0 < a.N, fc, out_base + f0, pol_b, pol_a);
       }
-      if (sm.u.slot >= 0) window_ticket_reduce<VEC, float>(a, sm.u.g, sm.u.slot, sm.u.rid, sm.u.avail, n_fc);
+      if (sm.u.window && sm.u.to_part)
+        window_ticket_reduce<VEC, float>(a, sm.u.g, a.s.grp_slot[sm.u.g], sm.u.rid, sm.u.avail, n_fc);
     }
     __syncwarp();
     u = sm.u.next;
@@ -940,10 +868,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
   }
 }
 
-template <int VEC, class BT, int kDepth, int MINB, bool kFull>
+template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap>
 int launch_stream_k(const SpmmArgs& a, cudaStream_t st) {
   static int blocks = 0;
-  auto kern = k_spmm_stream<VEC, BT, kDepth, MINB, kFull>;
+  auto kern = k_spmm_stream<VEC, BT, kDepth, MINB, kFull, kNoL1, kCap>;
   if (!blocks) {
     int per_sm = 0;
     RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
@@ -954,21 +882,28 @@ int launch_stream_k(const SpmmArgs& a, cudaStream_t st) {
   return launch_fixup<float>(a, st);
 }
 
-template <int VEC, class BT, int kDepth, int MINB>
+template <int VEC, class BT, int kDepth, int MINB, int kCap = 320>
 int launch_stream(const SpmmArgs& a, cudaStream_t st) {
-  if (a.N % (32 * VEC) == 0) return launch_stream_k<VEC, BT, kDepth, MINB, true>(a, st);
-  return launch_stream_k<VEC, BT, kDepth, MINB, false>(a, st);
+  const bool full = a.N % (32 * VEC) == 0;
+  if (a.flags & 256) {  // gathers bypass L1 allocation (tuning experiment)
+    if (full) return launch_stream_k<VEC, BT, kDepth, MINB, true, true, kCap>(a, st);
+    return launch_stream_k<VEC, BT, kDepth, MINB, false, true, kCap>(a, st);
+  }
+  if (full) return launch_stream_k<VEC, BT, kDepth, MINB, true, false, kCap>(a, st);
+  return launch_stream_k<VEC, BT, kDepth, MINB, false, false, kCap>(a, st);
 }
 
-// pipeline depth / occupancy variants (tuning knob: flags bits 3-5)
+// pipeline depth / occupancy / list-size variants (tuning knob: flags bits 3-5)
 template <int VEC, class BT>
 int dispatch_stream(const SpmmArgs& a, cudaStream_t st) {
   switch ((a.flags >> 3) & 7) {
     case 1: return launch_stream<VEC, BT, 4, 4>(a, st);
-    case 2: return launch_stream<VEC, BT, 12, 2>(a, st);
-    case 3: return launch_stream<VEC, BT, 16, 2>(a, st);
-    case 4: return launch_stream<VEC, BT, 8, 4>(a, st);
-    default: return launch_stream<VEC, BT, 8, 3>(a, st);
+    case 2: return launch_stream<VEC, BT, 6, 4>(a, st);  // the default (case 0)
+    case 3: return launch_stream<VEC, BT, 8, 3>(a, st);
+    case 4: return launch_stream<VEC, BT, 4, 4, 256>(a, st);
+    case 5: return launch_stream<VEC, BT, 6, 4, 256>(a, st);
+    case 6: return launch_stream<VEC, BT, 4, 4, 448>(a, st);
+    default: return launch_stream<VEC, BT, 6, 4>(a, st);
   }
 }
 
@@ -1090,43 +1025,6 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   return kOk;
 }
 
-size_t rsh_hot_columns_bytes(int64_t n_cols) {
-  Carve cv(nullptr);
-  cv.take<int32_t>(n_cols + 1);
-  cv.take<int32_t>(kDegBins);
-  cv.take<int64_t>(4);
-  return cv.used + 256;
-}
-
-// L2 residency plan for the B rows (see k_col_degree): fills the schedule's per-block hot masks.
-// row_bytes = N x sizeof(B element); budget_bytes = B bytes to keep L2-resident.  stats_out
-// (device int64[3], may be NULL) = [degree threshold, hot rows, gathers they serve].
-int rsh_hot_columns(int64_t n_rows, int64_t n_cols, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
-                    int64_t n_blocks, int64_t n_res, const int32_t* res_col_id, int64_t res_nnz, int64_t row_bytes,
-                    int64_t budget_bytes, void* sched, size_t sched_bytes, void* ws, size_t ws_bytes, int64_t* stats_out,
-                    cudaStream_t st) {
-  if (n_cols < 0 || n_blocks < 0 || res_nnz < 0 || row_bytes < 1 || budget_bytes < 0)
-    return fail(kInvalid, "rsh_hot_columns: bad sizes");
-  Sched s;
-  const size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
-  if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_hot_columns: schedule buffer too small");
-  if (!ws || ws_bytes < rsh_hot_columns_bytes(n_cols)) return fail(kInvalid, "rsh_hot_columns: workspace too small");
-  Carve cv(ws);
-  int32_t* deg = cv.take<int32_t>(n_cols + 1);
-  int32_t* hist = cv.take<int32_t>(kDegBins);
-  int64_t* stats = cv.take<int64_t>(4);
-  RSH_CUDA(cudaMemsetAsync(deg, 0, (n_cols + 1) * sizeof(int32_t), st));
-  RSH_CUDA(cudaMemsetAsync(hist, 0, kDegBins * sizeof(int32_t), st));
-  const unsigned g = 4 * (unsigned)sm_count();
-  if (n_blocks + res_nnz) k_col_degree<<<g, kThreads, 0, st>>>((const unsigned long long*)bitmaps, col_id, n_blocks, res_col_id, res_nnz, deg);
-  if (n_cols) k_deg_hist<<<g, kThreads, 0, st>>>(deg, n_cols, hist);
-  k_deg_threshold<<<1, 1, 0, st>>>(hist, row_bytes, budget_bytes, stats);
-  k_hot_masks<<<g, kThreads, 0, st>>>(col_id, n_blocks, deg, stats, s);
-  RSH_LAUNCHED("rsh_hot_columns");
-  if (stats_out) RSH_CUDA(cudaMemcpyAsync(stats_out, stats, 3 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-  return kOk;
-}
-
 // bytes of chunk-partial workspace rsh_spmm needs (partial_slots from the schedule header)
 size_t rsh_partials_bytes(int64_t partial_slots, int64_t N, int32_t accum) {
   return (size_t)(partial_slots > 0 ? partial_slots : 1) * 8 * (size_t)N * (accum ? sizeof(double) : sizeof(float));
@@ -1140,7 +1038,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 511) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 1023) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -1162,8 +1060,8 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.s = s;
   a.partials = partials;
   a.flags = accum >> 1;  // tuning knobs: bits 0-1 row-walk occupancy variant, bit 2 no L2 cache hints,
-                         // bits 3-5 stream depth/occupancy variant, bit 6 stream kernel instead of the row walk,
-                         // bit 7 ignore the hot-column L2 plan
+                         // bits 3-5 stream depth/occupancy variant, bit 6 row-walk kernel instead of the stream,
+                         // bit 8 stream gathers bypass L1 allocation
   accum &= 1;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;
@@ -1172,24 +1070,25 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                      ((uintptr_t)B % (vec * esz)) || ((uintptr_t)C % (vec * 4 < 16 ? vec * 4 : 16))))
     vec >>= 1;
   if (accum == 1 && vec > 4) vec = 4;
-  if ((uintptr_t)col_id & 15) a.flags &= ~64;  // the stream kernel reads col_id slots as int4
-  if (accum == 0 && (a.flags & 64)) {
-    // streaming kernel (flags bit 6)
+  // the stream kernel addresses B rows with a 32-bit byte stride
+  if (ldb * (int64_t)esz >= (1LL << 32)) a.flags |= 64;
+  if (accum == 0 && !(a.flags & 64)) {
+    // streaming kernel: the f32-accumulation default (flags bit 6 selects the row-walk kernel)
     if (b_dtype == 0) {
       if (vec >= 4) return dispatch_stream<4, float>(a, st);
       if (vec == 2) return dispatch_stream<2, float>(a, st);
-      return launch_stream<1, float, 8, 3>(a, st);
+      return launch_stream<1, float, 6, 4>(a, st);
     }
     if (b_dtype == 1) {
       if (vec == 8) return dispatch_stream<8, __nv_bfloat16>(a, st);
-      if (vec == 4) return launch_stream<4, __nv_bfloat16, 8, 3>(a, st);
-      if (vec == 2) return launch_stream<2, __nv_bfloat16, 8, 3>(a, st);
-      return launch_stream<1, __nv_bfloat16, 8, 3>(a, st);
+      if (vec == 4) return launch_stream<4, __nv_bfloat16, 6, 4>(a, st);
+      if (vec == 2) return launch_stream<2, __nv_bfloat16, 6, 4>(a, st);
+      return launch_stream<1, __nv_bfloat16, 6, 4>(a, st);
     }
     if (vec == 8) return dispatch_stream<8, __half>(a, st);
-    if (vec == 4) return launch_stream<4, __half, 8, 3>(a, st);
-    if (vec == 2) return launch_stream<2, __half, 8, 3>(a, st);
-    return launch_stream<1, __half, 8, 3>(a, st);
+    if (vec == 4) return launch_stream<4, __half, 6, 4>(a, st);
+    if (vec == 2) return launch_stream<2, __half, 6, 4>(a, st);
+    return launch_stream<1, __half, 6, 4>(a, st);
   }
   if (accum == 0 && b_dtype == 0 && (N == 64 || N == 32) && ldb % 4 == 0 && ldc % 4 == 0 && !((uintptr_t)B & 15) &&
       !((uintptr_t)C & 15)) {

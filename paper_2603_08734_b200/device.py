@@ -295,24 +295,6 @@ class SpmmPlan:
         h = hdr.cpu().tolist()
         self.groups, self.window_units, self.units, self.partial_slots, self.uncovered = h[:5]
         self._partials = {}
-        self.hot_key = None
-        self.hot_stats = None
-
-    def ensure_hot(self, t: "DeviceTile", row_bytes: int, budget: int | None = None, stream=None) -> None:
-        """L2 residency plan for B rows of ``row_bytes`` (rsh_hot_columns), computed once per row
-        size; budget defaults to HOT_BUDGET_FRAC of the device L2."""
-        if budget is None:
-            budget = int(os.environ.get("RSH_HOT_BUDGET", 0)) or int(HOT_BUDGET_FRAC * _l2_bytes(t.device))
-        key = (row_bytes, budget)
-        if self.hot_key == key:
-            return
-        ws = _ws(lib().rsh_hot_columns_bytes(t.n_cols), t.device)
-        stats = torch.zeros(3, dtype=torch.int64, device=t.device)
-        call("rsh_hot_columns", t.n_rows, t.n_cols, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id), t.n_blocks, t.n_res,
-             _ptr(t.res_col_id), int(t.res_col_id.numel()), row_bytes, budget, _ptr(self.buf), self.nbytes, _ptr(ws),
-             ws.numel(), _ptr(stats), _stream(stream))
-        self.hot_stats = stats.cpu().tolist()
-        self.hot_key = key
 
     def partials(self, N: int, accum: int, dev) -> torch.Tensor:
         key = (N, accum)
@@ -324,15 +306,6 @@ class SpmmPlan:
 
 # rsh_spmm_cc tuning knobs (accum bits 1..): development override through RSH_CC_VARIANT
 CC_VARIANT = int(os.environ.get("RSH_CC_VARIANT", "0"))
-HOT_BUDGET_FRAC = 0.5  # share of L2 planned for evict_last B rows (the rest: C / format streams)
-_L2 = {}
-
-
-def _l2_bytes(dev) -> int:
-    i = dev.index if dev.index is not None else torch.cuda.current_device()
-    if i not in _L2:
-        _L2[i] = int(getattr(torch.cuda.get_device_properties(i), "L2_cache_size", 0)) or (126 << 20)
-    return _L2[i]
 
 
 def spmm_plan(t: DeviceTile, chunk: int = CHUNK_CC) -> SpmmPlan:
@@ -354,25 +327,25 @@ def tc_eligible(t: DeviceTile, b: torch.Tensor, accumulate: str = "f32") -> bool
 
 
 def resolve_math(math: str, b: torch.Tensor, t: DeviceTile, accumulate: str) -> str:
-    """"tc" (tcgen05 window path) or "cc" (CUDA-core FP32 FMA).  fp32 B: exact FP32 unless the
-    caller asks for tf32; bf16 / f16 B: products are exact either way, so the tensor cores run
-    whenever the shape allows."""
-    if math == "fp32" or accumulate != "f32":
+    """"tc" (tcgen05 window path) or "cc" (CUDA-core streaming kernel).  "auto" runs the CUDA
+    cores for every dtype: the window path's cost is the B-row gather, and the streaming kernel
+    gathers faster than the tensor-core pipeline can stage (measured on every BASELINE config,
+    DESIGN.md section 3.3).  "tf32" / "tc" ask for the tensor cores (TF32 for fp32 B, BF16/FP16
+    MMA for half B); "fp32" is the exact-FP32 CUDA-core path."""
+    if math not in ("auto", "fp32", "tf32", "tc"):
+        raise ValueError(f"unknown math mode {math!r}")
+    if math in ("auto", "fp32") or accumulate != "f32":
         return "cc"
     if not tc_eligible(t, b, accumulate):
-        if math == "tf32":
-            raise ValueError("math='tf32' needs N in {128, 256}, f32 accumulation and 16-byte aligned B rows")
-        return "cc"
-    if math == "tf32":
-        return "tc"
-    return "tc" if b.dtype in (torch.bfloat16, torch.float16) else "cc"
+        raise ValueError(f"math={math!r} needs N in {{128, 256}}, f32 accumulation and 16-byte aligned B rows")
+    return "tc"
 
 
 def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None, accumulate: str = "f32",
-                stream=None, math: str = "auto", l1: bool = True, cc_variant: int | None = None, hot: bool = True) -> torch.Tensor:
+                stream=None, math: str = "auto", l1: bool = True, cc_variant: int | None = None) -> torch.Tensor:
     """C = A @ B with A an RS-Tile on device; B [n_cols, N] f32/bf16/f16 row-major on device.
     Returns (or fills) C [n_rows, N] float32.  accumulate: "f32" | "f64" (execute.py:33-49);
-    math: "auto" | "fp32" (CUDA-core FMA) | "tf32" (tensor cores, see resolve_math)."""
+    math: "auto" / "fp32" (CUDA-core FMA) | "tf32" / "tc" (tensor cores, see resolve_math)."""
     if b.dim() != 2 or b.shape[0] != t.n_cols:
         raise ValueError(f"dimension mismatch: matrix has {t.n_cols} columns, B has {tuple(b.shape)}")
     if b.dtype not in _BDT:
@@ -393,8 +366,6 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
         cc_variant = CC_VARIANT
     path = resolve_math(math, b, t, accumulate)
     plan = spmm_plan(t, CHUNK_TC if path == "tc" else CHUNK_CC)
-    if path == "cc" and hot:
-        plan.ensure_hot(t, N * b.element_size(), stream=stream)
     part = plan.partials(N, acc, b.device)
     call("rsh_spmm_tc" if path == "tc" else "rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
          _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),

@@ -37,8 +37,9 @@ class ExecConfig:
     """execute.py:33-49 plus the GPU arithmetic mode.
 
     math: "fp32"  CUDA-core FP32 FMA (exact f32 products; the reference's f32 semantics)
-          "tf32"  tensor-core window path, TF32 operands, f32 accumulation (north-star (2))
-          "auto"  fp32 unless the caller opts into tf32
+          "tf32"  tensor-core window path, TF32 operands, f32 accumulation (north-star (2));
+                  "tc" is the same request for any B dtype (BF16/FP16 MMA for half B)
+          "auto"  the CUDA-core streaming kernel for every dtype (the faster path, measured)
     """
 
     num_workers: int = 1
@@ -52,8 +53,8 @@ class ExecConfig:
         if self.accumulate_precision not in ("f32", "f64"):
             raise ValueError(
                 f"accumulate_precision must be f32 or f64, got {self.accumulate_precision!r}")
-        if self.math not in ("auto", "fp32", "tf32"):
-            raise ValueError(f"math must be auto, fp32 or tf32, got {self.math!r}")
+        if self.math not in ("auto", "fp32", "tf32", "tc"):
+            raise ValueError(f"math must be auto, fp32, tf32 or tc, got {self.math!r}")
 
     @property
     def dtype(self) -> np.dtype:

@@ -8,6 +8,7 @@ reference's TcPart / ResidualPart / RsTileMatrix types, bit-exact with the refer
 
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -288,6 +289,112 @@ def decode_rstile(m: RsTileMatrix) -> CsrMatrix:
         raise FormatError(f"decoded arrays are not canonical: {exc}") from exc
 
 
-__all__ = ["FormatError", "TcPart", "ResidualPart", "RsTileMatrix", "build_rstile",
-           "build_rstile_device", "decode_rstile", "decode_rstile_device", "tile_from_device",
-           "tile_to_device", "validate_rstile", "validate_rstile_device"]
+# ---------------------------------------------------------------------------------------------
+# serialization (tile.py:314-388) and storage accounting (tile.py:394-440)
+# ---------------------------------------------------------------------------------------------
+
+RSTILE_MAGIC = b"RSTL"
+RSTILE_VERSION = 1
+# magic, version, window_size, n_rows, n_cols, entries, blocks, tc nnz, residual rows, residual nnz
+_HEADER = struct.Struct("<4sHHIIIQQIQ")
+HEADER_BYTES = _HEADER.size
+# on-disk dtypes of the nine arrays, in file order (offsets are stored as u32)
+_FILE_LAYOUT = (("tc", "row_window_id", "<u4"), ("tc", "row_window_offset", "<u4"), ("tc", "bitmaps", "<u8"),
+                ("tc", "col_id", "<u4"), ("tc", "values", "<f4"), ("residual", "row_id", "<u4"),
+                ("residual", "row_nnz_offset", "<u4"), ("residual", "col_id", "<u4"),
+                ("residual", "values", "<f4"))
+
+
+def rstile_bytes(m: RsTileMatrix) -> bytes:
+    """The .rst byte image of a format (no validation): the reference's header then the nine
+    arrays little-endian, offsets narrowed to u32 exactly as tile.py:318-341 writes them."""
+    tc, res = m.tc, m.residual
+    head = _HEADER.pack(RSTILE_MAGIC, RSTILE_VERSION, m.window_size, m.n_rows, m.n_cols, tc.n_entries,
+                        tc.n_blocks, tc.values.size, res.n_rows, res.values.size)
+    return head + b"".join(getattr(getattr(m, part), name).astype(dt).tobytes() for part, name, dt in _FILE_LAYOUT)
+
+
+def save_rstile(path, m: RsTileMatrix) -> None:
+    """tile.py:314-341: validate (on device), then write the .rst file."""
+    issues = validate_rstile(m)
+    if issues:
+        raise FormatError(issues[0])
+    with open(path, "wb") as fh:
+        fh.write(rstile_bytes(m))
+
+
+def save_rstile_device(path, t) -> None:
+    """Serialize a DeviceTile: validated in HBM, then copied out once and written."""
+    issues = validate_rstile_device(t)
+    if issues:
+        raise FormatError(issues[0])
+    with open(path, "wb") as fh:
+        fh.write(rstile_bytes(tile_from_device(t)))
+
+
+def parse_rstile(blob: bytes, name: str = "<bytes>") -> RsTileMatrix:
+    """The structural half of load_rstile (tile.py:344-382): header, sizes, truncation and
+    trailing-byte checks, with the reference's messages.  No semantic validation."""
+    if len(blob) < _HEADER.size:
+        raise FormatError(f"{name}: truncated header")
+    magic, version, wsize, n_rows, n_cols, entries, blocks, tc_nnz, r_rows, r_nnz = _HEADER.unpack_from(blob)
+    if magic != RSTILE_MAGIC:
+        raise FormatError(f"{name}: bad magic {magic!r}")
+    if version != RSTILE_VERSION:
+        raise FormatError(f"{name}: unsupported version {version}")
+    pos = _HEADER.size
+    fields = []
+    for count, dt in ((entries, "<u4"), (entries + 1, "<u4"), (blocks, "<u8"), (blocks * 8, "<u4"),
+                      (tc_nnz, "<f4"), (r_rows, "<u4"), (r_rows + 1, "<u4"), (r_nnz, "<u4"), (r_nnz, "<f4")):
+        width = int(count) * np.dtype(dt).itemsize
+        if pos + width > len(blob):
+            raise FormatError(f"{name}: truncated at byte {pos}")
+        fields.append(np.frombuffer(blob, dtype=dt, count=int(count), offset=pos))
+        pos += width
+    if pos != len(blob):
+        raise FormatError(f"{name}: {len(blob) - pos} trailing bytes")
+    return RsTileMatrix(n_rows, n_cols, TcPart(*fields[:5]), ResidualPart(*fields[5:]), wsize)
+
+
+def load_rstile(path) -> RsTileMatrix:
+    """tile.py:344-388: parse, then validate on device (FormatError with the first issue)."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    m = parse_rstile(blob, str(path))
+    issues = validate_rstile(m)
+    if issues:
+        raise FormatError(f"{path}: {issues[0]}")
+    return m
+
+
+@dataclass(frozen=True)
+class StorageReport:
+    """tile.py:398-407."""
+
+    coo_bytes: int
+    csr_bytes: int
+    rstile_bytes: int
+    tc_bytes: int
+    residual_bytes: int
+    bitmap_bytes: int
+    colid_bytes: int
+    offset_bytes: int
+
+
+def storage_report(a: CsrMatrix, m: RsTileMatrix) -> StorageReport:
+    """tile.py:410-440: byte counts under 32-bit indices, 32-bit values, 64-bit bitmaps; the
+    .rst file is exactly HEADER_BYTES + rstile_bytes."""
+    entries, blocks = m.tc.n_entries, m.tc.n_blocks
+    r_rows, r_nnz = m.residual.n_rows, int(m.residual.values.size)
+    bitmap_bytes, colid_bytes, offset_bytes = blocks * 8, blocks * 32, (entries + 1) * 4
+    tc_bytes = entries * 4 + offset_bytes + bitmap_bytes + colid_bytes + int(m.tc.values.size) * 4
+    residual_bytes = r_rows * 4 + r_nnz * 8 + (r_rows + 1) * 4
+    return StorageReport(coo_bytes=a.nnz * 12, csr_bytes=a.nnz * 8 + (a.n_rows + 1) * 4,
+                         rstile_bytes=tc_bytes + residual_bytes, tc_bytes=tc_bytes, residual_bytes=residual_bytes,
+                         bitmap_bytes=bitmap_bytes, colid_bytes=colid_bytes, offset_bytes=offset_bytes)
+
+
+__all__ = ["FormatError", "HEADER_BYTES", "RSTILE_MAGIC", "RSTILE_VERSION", "ResidualPart", "RsTileMatrix",
+           "StorageReport", "TcPart", "build_rstile", "build_rstile_device", "decode_rstile", "decode_rstile_device",
+           "load_rstile", "parse_rstile", "rstile_bytes", "save_rstile", "save_rstile_device", "storage_report",
+           "tile_from_device", "tile_to_device", "validate_rstile", "validate_rstile_device"]

@@ -71,9 +71,9 @@ def test_products_against_fp64_oracle(config):
     c_fp32_again = spmm_device(t, bt, math="fp32")
     assert torch.equal(c_fp32, c_fp32_again)
     use_tc = w.n_features in (128, 256)
-    c_tc = spmm_device(t, bt, math="tf32" if w.dtype == "f32" else "auto") if use_tc else None
+    c_tc = spmm_device(t, bt, math="tc") if use_tc else None
     if c_tc is not None:
-        assert torch.equal(c_tc, spmm_device(t, bt, math="tf32" if w.dtype == "f32" else "auto"))
+        assert torch.equal(c_tc, spmm_device(t, bt, math="tc"))
     # exact zeros on rows without nonzeros, over the whole C
     empty = torch.from_numpy(np.diff(np.asarray(a.row_ptr)) == 0).cuda()
     assert not c_fp32[empty].any()

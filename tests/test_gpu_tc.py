@@ -56,8 +56,9 @@ def test_half_operands_on_tensor_cores(dt, d):
     a = synth.generate_power_law(700, 500, 9000, 1.5, seed=3)
     t = _tile(a)
     b = _b(500, d, 5, getattr(torch, dt))
-    assert resolve_math("auto", b, t, "f32") == "tc"
-    c = spmm_device(t, b).cpu().numpy()
+    assert resolve_math("auto", b, t, "f32") == "cc"  # the streaming CUDA-core kernel is faster
+    assert resolve_math("tc", b, t, "f32") == "tc"
+    c = spmm_device(t, b, math="tc").cpu().numpy()
     _, ref64 = O.spmm_f64(O.Csr.of(a), b.float().cpu().numpy())
     err = O.rel_frobenius(c, ref64)
     assert err <= HALF_TOL

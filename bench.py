@@ -219,15 +219,17 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--math", default="auto", choices=["auto", "fp32", "tf32", "tc"])
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-shard path even on one GPU (config 5 at N=1 under torchrun)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.sharded:
         from paper_2603_08734_b200.dist import run_sharded_bench
-        run_sharded_bench(args, METRIC)
+        run_sharded_bench(args, METRIC, clock_factory=ClockSampler)
         return
     run_single(args)
 

@@ -542,10 +542,14 @@ int rsh_build_fill(const int64_t* row_ptr, const int32_t* col_idx, const float* 
         tc_values);
     RSH_LAUNCHED("k_values");
   }
-  if (chunk) {
-    k_entries<<<grid_1d(n_win > 0 ? n_win : 1), kThreads, 0, st>>>(win_start, n_win, block_base, chunk, entry_base,
-                                                                    row_window_id, row_window_offset);
+  if (chunk && n_win) {
+    k_entries<<<grid_1d(n_win), kThreads, 0, st>>>(win_start, n_win, block_base, chunk, entry_base, row_window_id,
+                                                   row_window_offset);
     RSH_LAUNCHED("k_entries");
+  } else if (n_win == 0 && row_window_offset) {
+    // no windows: the entry arrays are empty and row_window_offset = [0] (callers may pass a NULL
+    // chunk here, as torch hands out address 0 for empty tensors)
+    RSH_CUDA(cudaMemsetAsync(row_window_offset, 0, sizeof(int64_t), st));
   }
   return kOk;
 }

@@ -123,7 +123,7 @@ def rmat_device(scale: int, edge_factor: int, seed: int, device, a=0.57, b=0.19,
 # the sharded benchmark (bench.py --gpus N under torchrun)
 # ---------------------------------------------------------------------------------------------
 
-def run_sharded_bench(args, metric: str) -> None:
+def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
     import torch
     import torch.distributed as dist
     from .device import DeviceCsr, fill_tile, partition_device, plan_windows, spmm_device, spmm_plan
@@ -193,12 +193,22 @@ def run_sharded_bench(args, metric: str) -> None:
         spmm_device(tile, b, out=out)
     dist.barrier()
     torch.cuda.synchronize()
+    clocks = clock_factory(local) if (clock_factory is not None and rank == 0) else None
+    if clocks is not None:
+        clocks.start()
+        time.sleep(0.3)
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
     g0.record()
     for _ in range(args.steps):
         spmm_device(tile, b, out=out)
     g1.record()
     torch.cuda.synchronize()
+    w1 = time.time()
+    clk = None
+    if clocks is not None:
+        clocks.window = (w0, w1)
+        clk = clocks.stop()
     dist.barrier()
     local_ms = g0.elapsed_time(g1)
     tmax = torch.tensor([local_ms], dtype=torch.float64, device=dev)
@@ -227,7 +237,7 @@ def run_sharded_bench(args, metric: str) -> None:
             "gpu_launches": args.steps,
             "collectives": {"b_broadcast_ms": bcast_ms, "c_gather_ms": gather_ms,
                             "b_bytes": int(b.numel() * 4), "c_bytes": int(n * n_feat * 4)},
-            "e2e": None, "cpu_baseline": None,
+            "e2e": None, "cpu_baseline": None, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -135,6 +135,8 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # NCCL's banner / debug output goes to stderr: rank 0's stdout carries only the JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     dist.init_process_group("nccl", device_id=dev)
     w = synth.WORKLOADS[args.workload]
     n_feat = w.n_features

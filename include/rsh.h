@@ -83,6 +83,14 @@ int rsh_permute_rows(const int64_t* row_ptr, const int32_t* col_idx, const float
                      const int64_t* order, int64_t* out_row_ptr, int32_t* out_col_idx, float* out_values, void* ws,
                      size_t ws_bytes, cudaStream_t stream);
 
+/* ---- transpose: A^T as a canonical CSR (the GNN backward operand; no
+ *      reference counterpart -- the reference has no autograd).  Deterministic (stable radix
+ *      sort by column).  nnz and n_rows must fit int32. ------------------------------------ */
+size_t rsh_transpose_workspace(int64_t n_rows, int64_t n_cols, int64_t nnz);
+int rsh_transpose_csr(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
+                      int64_t n_cols, int64_t nnz, int64_t* out_row_ptr, int32_t* out_col_idx, float* out_values,
+                      void* ws, size_t ws_bytes, cudaStream_t stream);
+
 /* ---- persistent-kernel schedule: execute.py:136-168 (_window_groups, value starts) as device
  *      data.  Logical windows are cut into units of chunk_blocks blocks (>= 32; rsh_spmm_cc is
  *      tuned for 32, rsh_spmm_tc for 256) at fixed offsets, so results never depend on the

@@ -37,6 +37,8 @@ SIGNATURES = {
     "rsh_residual_gather": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "rsh_permute_workspace": (_sz, [_i64]),
     "rsh_permute_rows": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "rsh_transpose_workspace": (_sz, [_i64, _i64, _i64]),
+    "rsh_transpose_csr": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "rsh_schedule_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "rsh_schedule": (ctypes.c_int, [_i64, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]),
     "rsh_partials_bytes": (_sz, [_i64, _i64, _i32]),

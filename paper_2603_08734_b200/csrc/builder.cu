@@ -392,6 +392,40 @@ size_t partition_layout(void* base, int64_t n, PartitionWs* o) {
 
 }  // namespace
 
+namespace rsh {
+
+// ------------------------------------------------------------------------------------------
+// transpose (for the GNN backward pass): A^T as a canonical CSR.  A stable radix
+// sort of the nonzeros by column keeps them in row order inside every column, so each row of
+// A^T lists its columns (A's rows) strictly increasing -- the canonical CSR the builder expects.
+// ------------------------------------------------------------------------------------------
+
+__global__ void k_row_ids(const int64_t* __restrict__ rp, int64_t n_rows, int32_t* rid) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t p = rp[r]; p < rp[r + 1]; ++p) rid[p] = (int32_t)r;
+}
+
+__global__ void k_iota32(int32_t* x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = (int32_t)i;
+}
+
+__global__ void k_col_counts(const int32_t* __restrict__ col, int64_t nnz, int64_t* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)(cnt + col[i]), 1ull);
+}
+
+__global__ void k_transpose_gather(const int32_t* __restrict__ perm, const int32_t* __restrict__ rid,
+                                   const float* __restrict__ values, int64_t nnz, int32_t* out_col, float* out_val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = perm[i];
+    out_col[i] = rid[p];
+    out_val[i] = values[p];
+  }
+}
+
+}  // namespace rsh
+
 extern "C" {
 
 size_t rsh_partition_workspace(int64_t n_rows) {
@@ -654,6 +688,62 @@ int rsh_permute_rows(const int64_t* row_ptr, const int32_t* col_idx, const float
                                                             out_col_idx, out_values);
     RSH_LAUNCHED("k_perm_copy");
   }
+  return kOk;
+}
+
+size_t rsh_transpose_workspace(int64_t n_rows, int64_t n_cols, int64_t nnz) {
+  rsh::Carve cv(nullptr);
+  cv.take<int32_t>(nnz + 1);  // row id per nonzero
+  cv.take<int32_t>(nnz + 1);  // sorted keys
+  cv.take<int32_t>(nnz + 1);  // identity
+  cv.take<int32_t>(nnz + 1);  // permutation
+  cv.take<int64_t>(n_cols + 1);
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                  (int)(nnz > 0 ? nnz : 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, (int)(n_cols + 1));
+  cv.take<char>(a > b ? a : b);
+  (void)n_rows;
+  return cv.used + 256;
+}
+
+// A^T of a canonical CSR A (n_rows x n_cols): out_row_ptr[n_cols+1], out_col_idx[nnz],
+// out_values[nnz]; canonical (strictly increasing columns per row), deterministic.
+int rsh_transpose_csr(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
+                      int64_t n_cols, int64_t nnz, int64_t* out_row_ptr, int32_t* out_col_idx, float* out_values,
+                      void* ws, size_t ws_bytes, cudaStream_t st) {
+  using namespace rsh;
+  if (n_rows < 0 || n_cols < 0 || nnz < 0 || nnz >= (1LL << 31) || n_rows >= (1LL << 31))
+    return fail(kInvalid, "rsh_transpose_csr: bad sizes (nnz and rows must fit int32)");
+  const size_t need = rsh_transpose_workspace(n_rows, n_cols, nnz);
+  if (!ws || ws_bytes < need) return fail(kInvalid, "rsh_transpose_csr: workspace too small");
+  Carve cv(ws);
+  int32_t* rid = cv.take<int32_t>(nnz + 1);
+  int32_t* keys = cv.take<int32_t>(nnz + 1);
+  int32_t* iota = cv.take<int32_t>(nnz + 1);
+  int32_t* perm = cv.take<int32_t>(nnz + 1);
+  int64_t* cnt = cv.take<int64_t>(n_cols + 1);
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                  (int)(nnz > 0 ? nnz : 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, (int)(n_cols + 1));
+  size_t cb = a > b ? a : b;
+  void* tmp = cv.take<char>(cb);
+  RSH_CUDA(cudaMemsetAsync(cnt, 0, (n_cols + 1) * sizeof(int64_t), st));
+  if (nnz) {
+    k_col_counts<<<grid_1d(nnz), kThreads, 0, st>>>(col_idx, nnz, cnt);
+    k_row_ids<<<grid_1d(n_rows), kThreads, 0, st>>>(row_ptr, n_rows, rid);
+    k_iota32<<<grid_1d(nnz), kThreads, 0, st>>>(iota, nnz);
+    RSH_LAUNCHED("transpose prep");
+    int bits = 1;
+    while (bits < 31 && (1LL << bits) < n_cols) ++bits;
+    size_t t = cb;
+    RSH_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, col_idx, keys, iota, perm, (int)nnz, 0, bits, st));
+    k_transpose_gather<<<grid_1d(nnz), kThreads, 0, st>>>(perm, rid, values, nnz, out_col_idx, out_values);
+    RSH_LAUNCHED("k_transpose_gather");
+  }
+  size_t t = cb;
+  RSH_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t, cnt, out_row_ptr, (int)(n_cols + 1), st));
   return kOk;
 }
 

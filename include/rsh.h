@@ -91,6 +91,27 @@ int rsh_transpose_csr(const int64_t* row_ptr, const int32_t* col_idx, const floa
                       int64_t n_cols, int64_t nnz, int64_t* out_row_ptr, int32_t* out_col_idx, float* out_values,
                       void* ws, size_t ws_bytes, cudaStream_t stream);
 
+/* ---- locality-aware row reordering (reorder.py:1-481).  Device: column
+ *      weights d^-alpha and row sums (reorder.py:33-42,73-76), candidates + top-k weighted-Jaccard
+ *      kNN through A^T (reorder.py:158-230), objective terms, windowed 2-opt sweeps
+ *      (reorder.py:328-380).  Host (plain host pointers): Kruskal forest + DFS order
+ *      (reorder.py:268-321) and the objective's left-to-right sum. ------------------------- */
+size_t rsh_reorder_workspace(int64_t n_rows, int64_t n_cols);
+int rsh_column_weights(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                       double alpha, double* w, double* wsum, void* ws, size_t ws_bytes, cudaStream_t stream);
+int rsh_knn(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, const int64_t* at_row_ptr,
+            const int32_t* at_col_idx, const double* w, const double* wsum, int32_t k, int32_t max_candidates,
+            int64_t hub_cap, int32_t* nbr, double* nsim, int32_t* ncount, unsigned long long* stats,
+            cudaStream_t stream);
+int rsh_pair_dis(const int64_t* row_ptr, const int32_t* col_idx, const double* w, const double* wsum,
+                 const int64_t* order, int64_t m, double* dis, cudaStream_t stream);
+int rsh_two_opt_sweep(const int64_t* row_ptr, const int32_t* col_idx, const double* w, const double* wsum,
+                      int64_t* order, int64_t m, int32_t window, int64_t offset, unsigned long long* improved,
+                      cudaStream_t stream);
+int rsh_mst_order(int64_t m, int32_t k, const int32_t* nbr, const double* nsim, const int32_t* ncount,
+                  int64_t* order_out);
+double rsh_sum_sequential(const double* x, int64_t n);
+
 /* ---- persistent-kernel schedule: execute.py:136-168 (_window_groups, value starts) as device
  *      data.  Logical windows are cut into units of chunk_blocks blocks (>= 32; rsh_spmm_cc is
  *      tuned for 32, rsh_spmm_tc for 256) at fixed offsets, so results never depend on the

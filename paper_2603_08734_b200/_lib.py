@@ -39,6 +39,13 @@ SIGNATURES = {
     "rsh_permute_rows": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "rsh_transpose_workspace": (_sz, [_i64, _i64, _i64]),
     "rsh_transpose_csr": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "rsh_reorder_workspace": (_sz, [_i64, _i64]),
+    "rsh_column_weights": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp, _sz, _vp]),
+    "rsh_knn": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "rsh_pair_dis": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "rsh_two_opt_sweep": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i64, _vp, _vp]),
+    "rsh_mst_order": (ctypes.c_int, [_i64, _i32, _vp, _vp, _vp, _vp]),
+    "rsh_sum_sequential": (_f64, [_vp, _i64]),
     "rsh_schedule_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "rsh_schedule": (ctypes.c_int, [_i64, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]),
     "rsh_partials_bytes": (_sz, [_i64, _i64, _i32]),

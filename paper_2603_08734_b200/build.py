@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librsh.so")
-SOURCES = ["capi.cu", "builder.cu", "spmm_cc.cu", "spmm_tc.cu", "tile_ops.cu"]
+SOURCES = ["capi.cu", "builder.cu", "spmm_cc.cu", "spmm_tc.cu", "tile_ops.cu", "reorder.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -371,7 +371,7 @@ def run_single(args):
                                      "schedule": 1e3 * t_sched},
                    "format": {"entries": tile.n_entries, "blocks": tile.n_blocks, "residual_rows": tile.n_res,
                               "units": plan.units, "uncovered_rows": plan.uncovered}},
-        "gpu_launches": args.steps,
+        "gpu_launches": 3 * args.steps,  # per step: the SpMM kernel + the two long-window fix-up kernels
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(args.workload),
                      "algorithmic_bytes": alg_bytes, "kernel": kernel, "kernel_ms": kern_avg,

@@ -580,6 +580,10 @@ struct StreamSmem {
   UnitDesc u;
 };
 
+// format-stream copy with an L2 policy (the nonzero stream is read once: evict_first)
+__device__ __forceinline__ void cp_async4_sp(uint32_t saddr, const void* g, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(saddr), "l"(g), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async4_s(uint32_t saddr, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
 }
@@ -684,8 +688,13 @@ __device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>&
     const int pos = (int)((((i < 4 ? F0 : F1) >> (16 * (i & 3))) & 0xffffull)) + r;
     if (pos >= P0 && pos < P1) {
       const uint32_t d = list_s + (uint32_t)(pos - P0) * 8u;
-      cp_async4_s(d, cbase + (bit & 7));
-      cp_async4_s(d + 4, vbase + r);
+      if (a.flags & 1024) {
+        cp_async4_s(d, cbase + (bit & 7));
+        cp_async4_s(d + 4, vbase + r);
+      } else {
+        cp_async4_sp(d, cbase + (bit & 7), pol_a);
+        cp_async4_sp(d + 4, vbase + r, pol_a);
+      }
     }
     ++r;
   }
@@ -713,7 +722,7 @@ __device__ __forceinline__ void residual_fill(const SpmmArgs& a, StreamSmem<kCap
 // Entries are consumed in groups of kDepth: a group that stays inside the current row (the
 // common case) runs without any per-entry row test; only groups that reach a row end take the
 // per-entry path that stores finished rows.
-template <int VEC, class BT, int kDepth, bool kFull, bool kNoL1, int kCap>
+template <int VEC, class BT, int kDepth, bool kFull, bool kNoL1, int kCap, int kG>
 __device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem<kCap>& sm, const BT* __restrict__ Bf,
                                             bool active, int fc, float* __restrict__ out, uint64_t pol_b,
                                             uint64_t pol_a) {
@@ -721,11 +730,30 @@ __device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem<kCap>&
   const uint32_t rstride = (uint32_t)(a.ldb * (int64_t)sizeof(BT));  // bytes per B row (< 4 GiB, checked on the host)
   const int total = sm.u.total;
   const bool single = total <= kCap;
+  const int nrows = sm.u.nrows;
+  // kG lane groups (narrow rows: a group of 32/kG lanes covers all N features) stream disjoint
+  // row ranges of the unit, split where the running entry count crosses total * g / kG; every
+  // row is still summed by one group in list order
+  int r0 = 0, r1 = nrows;
+  if constexpr (kG > 1) {
+    const int g = (int)(threadIdx.x & 31) / (32 / kG);
+    const int t0 = (int)((int64_t)total * g / kG), t1 = (int)((int64_t)total * (g + 1) / kG);
+    r0 = 0;
+    r1 = 0;
+    for (int r = 0; r < nrows; ++r) {
+      const int e = sm.rend[r];
+      r0 += (g > 0 && e <= t0);
+      r1 += (e <= t1);
+    }
+    if (g == kG - 1) r1 = nrows;
+  }
+  const int gb = r0 ? sm.rend[r0 - 1] : 0;                 // this group's entries [gb, ge)
+  const int ge = r1 ? sm.rend[r1 - 1] : 0;
   float acc[VEC];
 #pragma unroll
   for (int t = 0; t < VEC; ++t) acc[t] = 0.f;
-  int cur = 0;
-  int nxt_end = sm.rend[0];
+  int cur = r0;
+  int nxt_end = sm.rend[cur];
   auto flush = [&]() {
     if (kFull || active) store_c<VEC, float>(out + sm.rowoff[cur], acc);
 #pragma unroll
@@ -746,14 +774,16 @@ __device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem<kCap>&
       else residual_fill<kCap>(a, sm, P0);
     }
     const int len = total - P0 < kCap ? total - P0 : kCap;
+    const int lb = gb - P0 > 0 ? gb - P0 : 0;              // this group's part of the piece
+    const int le = ge - P0 < len ? ge - P0 : len;
     RawVec<VEC, BT> rb[kDepth];
     float vv[kDepth];
 #pragma unroll
     for (int p = 0; p < kDepth; ++p)
-      if (p < len) issue(p, rb[p], vv[p]);
-    int base = 0;
-    // steady state: every refill index base + kDepth + p is inside the piece
-    for (; base + 2 * kDepth <= len; base += kDepth) {
+      if (lb + p < le) issue(lb + p, rb[p], vv[p]);
+    int base = lb;
+    // steady state: every refill index base + kDepth + p is inside the group's part
+    for (; base + 2 * kDepth <= le; base += kDepth) {
       if (P0 + base + kDepth - 1 < nxt_end) {
 #pragma unroll
         for (int p = 0; p < kDepth; ++p) {
@@ -769,30 +799,30 @@ __device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem<kCap>&
         }
       }
     }
-    // drain: the last one or two groups
-    for (; base < len; base += kDepth) {
+    // drain: the last one or two groups of entries
+    for (; base < le; base += kDepth) {
 #pragma unroll
       for (int p = 0; p < kDepth; ++p) {
         const int e = base + p;
-        if (e < len) {
+        if (e < le) {
           while (P0 + e >= nxt_end) flush();
           if (kFull || active) raw_fma<VEC, BT>(rb[p], vv[p], acc);
-          if (e + kDepth < len) issue(e + kDepth, rb[p], vv[p]);
+          if (e + kDepth < le) issue(e + kDepth, rb[p], vv[p]);
         }
       }
     }
   }
-  const int nrows = sm.u.nrows;
-  while (cur < nrows) flush();
+  while (cur < r1) flush();
 }
 
-template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap>
+template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap, int kG>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
   __shared__ StreamSmem<kCap> smem_all[kThreads / 32];
   StreamSmem<kCap>& sm = smem_all[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t total_units = a.s.header[2];
-  const int n_fc = (a.N + 32 * VEC - 1) / (32 * VEC);
+  // kG > 1: lane groups of 32/kG lanes, each covering all N = (32/kG) * VEC features
+  const int n_fc = kG > 1 ? 1 : (a.N + 32 * VEC - 1) / (32 * VEC);
   const BT* B = reinterpret_cast<const BT*>(a.B);
   const uint64_t pol_b = policy_evict_last(), pol_a = policy_evict_first();
 
@@ -847,8 +877,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
       }
       float* const out_base = sm.u.to_part ? reinterpret_cast<float*>(a.partials) : a.C;
       for (int fc = 0; fc < n_fc; ++fc) {
-        const int f0 = fc * 32 * VEC + lane * VEC;
-        stream_rows<VEC, BT, kDepth, kFull, kNoL1, kCap>(a, sm, B + f0, f0 < a.N, fc, out_base + f0, pol_b, pol_a);
+        const int f0 = kG > 1 ? (lane % (32 / kG)) * VEC : fc * 32 * VEC + lane * VEC;
+        stream_rows<VEC, BT, kDepth, kFull, kNoL1, kCap, kG>(a, sm, B + f0, f0 < a.N, fc, out_base + f0, pol_b,
+                                                            pol_a);
       }
       if (sm.u.window && sm.u.to_part)
         window_ticket_reduce<VEC, float>(a, sm.u.g, a.s.grp_slot[sm.u.g], sm.u.rid, sm.u.avail, n_fc);
@@ -868,10 +899,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
   }
 }
 
-template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap>
+template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap, int kG = 1>
 int launch_stream_k(const SpmmArgs& a, cudaStream_t st) {
   static int blocks = 0;
-  auto kern = k_spmm_stream<VEC, BT, kDepth, MINB, kFull, kNoL1, kCap>;
+  auto kern = k_spmm_stream<VEC, BT, kDepth, MINB, kFull, kNoL1, kCap, kG>;
   if (!blocks) {
     int per_sm = 0;
     RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
@@ -891,6 +922,12 @@ int launch_stream(const SpmmArgs& a, cudaStream_t st) {
   }
   if (full) return launch_stream_k<VEC, BT, kDepth, MINB, true, false, kCap>(a, st);
   return launch_stream_k<VEC, BT, kDepth, MINB, false, false, kCap>(a, st);
+}
+
+// narrow rows (N = 16 B x 32 lanes / kG): kG lane groups stream disjoint row ranges of a unit
+template <int VEC, class BT, int kG>
+int launch_stream_groups(const SpmmArgs& a, cudaStream_t st) {
+  return launch_stream_k<VEC, BT, 6, 4, true, false, 320, kG>(a, st);
 }
 
 // pipeline depth / occupancy / list-size variants (tuning knob: flags bits 3-5)
@@ -1038,7 +1075,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 1023) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 8191) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -1061,7 +1098,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.partials = partials;
   a.flags = accum >> 1;  // tuning knobs: bits 0-1 row-walk occupancy variant, bit 2 no L2 cache hints,
                          // bits 3-5 stream depth/occupancy variant, bit 6 row-walk kernel instead of the stream,
-                         // bit 8 stream gathers bypass L1 allocation
+                         // bit 8 stream gathers bypass L1 allocation, bit 10 list copies without L2 hint, bit 11 no lane groups
   accum &= 1;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;
@@ -1074,6 +1111,15 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   if (ldb * (int64_t)esz >= (1LL << 32)) a.flags |= 64;
   if (accum == 0 && !(a.flags & 64)) {
     // streaming kernel: the f32-accumulation default (flags bit 6 selects the row-walk kernel)
+    const bool al16 = !((uintptr_t)B & 15) && !((uintptr_t)C & 15) && (ldb * (int64_t)esz) % 16 == 0 && ldc % 4 == 0;
+    if (al16 && !(a.flags & 2048)) {  // narrow rows: 16-byte lanes in groups (flags bit 11 disables)
+      if (b_dtype == 0 && N == 64) return launch_stream_groups<4, float, 2>(a, st);
+      if (b_dtype == 0 && N == 32) return launch_stream_groups<4, float, 4>(a, st);
+      if (b_dtype == 1 && N == 128) return launch_stream_groups<8, __nv_bfloat16, 2>(a, st);
+      if (b_dtype == 1 && N == 64) return launch_stream_groups<8, __nv_bfloat16, 4>(a, st);
+      if (b_dtype == 2 && N == 128) return launch_stream_groups<8, __half, 2>(a, st);
+      if (b_dtype == 2 && N == 64) return launch_stream_groups<8, __half, 4>(a, st);
+    }
     if (b_dtype == 0) {
       if (vec >= 4) return dispatch_stream<4, float>(a, st);
       if (vec == 2) return dispatch_stream<2, float>(a, st);

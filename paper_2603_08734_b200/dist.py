@@ -236,7 +236,7 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
                        "n_features": n_feat, "parallelism": f"row shard x{world}",
                        "cuts": [int(x) for x in cuts], "preprocess_ms": 1e3 * t_build,
                        "l2": "no flush: inputs exceed the 126 MB L2"},
-            "gpu_launches": args.steps,
+            "gpu_launches": 3 * args.steps,  # per step: the SpMM kernel + the two long-window fix-up kernels
             "collectives": {"b_broadcast_ms": bcast_ms, "c_gather_ms": gather_ms,
                             "b_bytes": int(b.numel() * 4), "c_bytes": int(n * n_feat * 4)},
             "e2e": None, "cpu_baseline": None, "clocks": clk,

@@ -286,3 +286,31 @@ def test_permute_rows_matches_reference_semantics(small_corpus):
         assert O.tiles_equal(O.Tile.of(m), want) == []
     with pytest.raises(ValueError):
         P.Permutation(np.array([0, 0, 1]), 0.0)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_stream_kernel_bit_identical_across_variants(dtype):
+    """The streaming kernel's list pieces (kCap 256 / 320 / 448), pipeline depths and the row-walk
+    kernel accumulate every row in the same order: C must be bitwise equal across them (and
+    across lane-group splits of narrow rows, flag 2048),
+    including multi-chunk windows (partials + ticket / fix-up reduction) and a near-dense row."""
+    import torch
+    from paper_2603_08734_b200 import synth
+    from paper_2603_08734_b200.device import DeviceCsr, build_device, spmm_device
+    a = synth.generate_power_law(3000, 2500, 60000, 1.3, seed=21)
+    dense = np.zeros((a.n_rows, a.n_cols), np.float32)
+    rows = np.repeat(np.arange(a.n_rows), np.diff(np.asarray(a.row_ptr)))
+    dense[rows, np.asarray(a.col_idx)] = np.asarray(a.values)
+    rng = np.random.default_rng(4)
+    dense[17, rng.choice(a.n_cols, 2000, replace=False)] = rng.uniform(-1, 1, 2000).astype(np.float32)
+    a = P.CsrMatrix.from_dense(dense)
+    t = build_device(DeviceCsr.from_host(a))
+    for n in (64, 128, 256):
+        b = torch.from_numpy(rand_b(a.n_cols, n, n)).cuda().to(getattr(torch, dtype))
+        if dtype == "bfloat16" and n == 64:
+            continue
+        base = spmm_device(t, b, math="fp32", cc_variant=0)
+        # the row walk sums in the same order except its narrow-row (N <= 64 fp32) lane-group mode
+        for v in (8, 16, 24, 32, 40, 48, 1024, 2048) + ((64,) if n >= 128 or dtype != "float32" else ()):
+            got = spmm_device(t, b, math="fp32", cc_variant=v)
+            assert torch.equal(got.view(torch.int32), base.view(torch.int32)), (n, v)

@@ -123,10 +123,20 @@ def rmat_device(scale: int, edge_factor: int, seed: int, device, a=0.57, b=0.19,
 # the sharded benchmark (bench.py --gpus N under torchrun)
 # ---------------------------------------------------------------------------------------------
 
+def _hbm_peak() -> float:
+    """MEASURED_PEAKS.json hbm_gbs (driver-written), else the profiling recipe's fallback."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    try:
+        with open(os.path.join(root, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh).get("hbm_gbs", 6650.0))
+    except (OSError, ValueError, TypeError):
+        return 6650.0
+
+
 def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
     import torch
     import torch.distributed as dist
-    from .device import DeviceCsr, fill_tile, partition_device, plan_windows, spmm_device, spmm_plan
+    from .device import DeviceCsr, DeviceTile, fill_tile, partition_device, plan_windows, spmm_device, spmm_plan
     from .partition import estimate_thresholds
     from . import synth
 
@@ -135,9 +145,20 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # NCCL's banner / debug output goes to stderr: rank 0's stdout carries only the JSON line
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-    dist.init_process_group("nccl", device_id=dev)
+    # rank 0's stdout carries only the JSON line: whatever the communicator setup prints (the
+    # NCCL version banner) is routed to stderr at the file-descriptor level
+    import sys
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+        torch.cuda.synchronize()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
     w = synth.WORKLOADS[args.workload]
     n_feat = w.n_features
     if args.workload.startswith("rmat"):
@@ -227,6 +248,49 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
     gather_ms = c0.elapsed_time(c1)
     flops = 2.0 * nnz * n_feat
     ms = total_ms / args.steps
+
+    # roofline: SURVEY 8(d) algorithmic bytes of this rank's shard (nnz x (4 + 4) + touched B
+    # rows + C rows), summed over ranks, against world x the measured HBM bandwidth
+    touched = int(torch.unique(loc.col_idx).numel()) if loc.nnz else 0
+    alg = torch.tensor([loc.nnz * 8.0 + touched * n_feat * 4.0 + (r1 - r0) * n_feat * 4.0], dtype=torch.float64,
+                       device=dev)
+    dist.all_reduce(alg)
+    alg_bytes = float(alg.item())
+    peak = _hbm_peak() * world
+
+    # end to end through the public device API with host buffers: every step copies this rank's
+    # format and B in from pinned host memory and its C rows out (max over ranks)
+    host = {k: getattr(tile, k).cpu().pin_memory() for k in (
+        "row_window_id", "row_window_offset", "bitmaps", "col_id", "values", "res_row_id", "res_offset",
+        "res_col_id", "res_values")}
+    b_host = b.cpu().pin_memory()
+    c_host = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory()
+    dev_bufs = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+    b_dev2 = torch.empty_like(b_host, device=dev)
+    t2 = DeviceTile(tile.n_rows, tile.n_cols, tile.window_size, **dev_bufs)
+    t2._plan = tile._plan  # the schedule is part of the prebuilt operator, like the format
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_ms = []
+    for it in range(e2e_steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for k, v in host.items():
+            dev_bufs[k].copy_(v, non_blocking=True)
+        b_dev2.copy_(b_host, non_blocking=True)
+        spmm_device(t2, b_dev2, out=out)
+        c_host.copy_(out, non_blocking=True)
+        s1.record()
+        torch.cuda.synchronize()
+        if it:
+            e2e_ms.append(s0.elapsed_time(s1))
+    emax = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
+    dist.all_reduce(emax, op=dist.ReduceOp.MAX)
+    h2d = sum(v.numel() * v.element_size() for v in host.values()) + b_host.numel() * 4
+    hb = torch.tensor([float(h2d), float(c_host.numel() * 4)], dtype=torch.float64, device=dev)
+    dist.all_reduce(hb)
+    e2e_ms_max = float(emax.item())
     if rank == 0:
         line = {
             "metric": metric, "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
@@ -239,7 +303,15 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
             "gpu_launches": 3 * args.steps,  # per step: the SpMM kernel + the two long-window fix-up kernels
             "collectives": {"b_broadcast_ms": bcast_ms, "c_gather_ms": gather_ms,
                             "b_bytes": int(b.numel() * 4), "c_bytes": int(n * n_feat * 4)},
-            "e2e": None, "cpu_baseline": None, "clocks": clk,
+            "roofline": {"bound": "hbm", "achieved": alg_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg_bytes / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                         "algorithmic_bytes": alg_bytes, "kernel": "k_spmm_stream",
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs x {world}"},
+            "e2e": {"value": flops / (e2e_ms_max * 1e-3) / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(hb[1].item()),
+                    "ms_per_step": e2e_ms_max,
+                    "path": "spmm_device per rank, pinned host shard format + B in, C shard out (max over ranks)"},
+            "cpu_baseline": None, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -124,6 +124,15 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
                  int64_t* header_out, cudaStream_t stream);
 size_t rsh_partials_bytes(int64_t partial_slots, int64_t n_features, int32_t accum);
 
+/* ---- row-major window list (optional, once per schedule; no reference counterpart): the
+ *      window units' nonzeros as int2 (col_id, value) pairs in stream order, 8 bytes per tc
+ *      nonzero (8-byte aligned).  rsh_spmm_cc then copies each unit's list coalesced instead of
+ *      decoding bitmaps; results are bit-identical with or without it.  The list must outlive
+ *      the schedule's use (its address is recorded in the schedule). */
+int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
+                          const float* tc_values, int64_t n_blocks, int64_t tc_nnz, int64_t n_res, void* sched,
+                          size_t sched_bytes, void* ulist, size_t ulist_bytes, cudaStream_t stream);
+
 /* ---- hybrid SpMM: execute.py:155-218 hybrid_spmm.  C[n_rows x N] (row stride ldc) is
  *      fully written: window rows assigned, residual rows assigned, all other rows zero.
  *      B[n_cols x N] row stride ldb; b_dtype 0 f32, 1 bf16, 2 f16; accum 0 f32, 1 f64.

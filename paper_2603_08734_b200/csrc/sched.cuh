@@ -21,6 +21,8 @@ enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
 // header: int64 [0]=groups [1]=window units [2]=all units [3]=partial slots [4]=uncovered rows
 //         [5]=blocks per window unit (the fixed chunking) [6]=windows reduced by the fixup
 //         kernels (more than kTicketMax chunks) [7]=their first-level fix-up segments
+//         [8]=device address of the row-major window list (rsh_schedule_rowmajor), [9]=its tc nnz
+//         (0 = no list)
 // counters: uint32 [0]=next unit [1]=warps done
 struct Sched {
   int64_t* header;
@@ -44,7 +46,7 @@ struct Sched {
 inline size_t sched_layout(void* base, int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res, Sched* s) {
   Carve cv(base);
   int64_t E = n_entries;
-  s->header = cv.take<int64_t>(8);
+  s->header = cv.take<int64_t>(16);
   s->counters = cv.take<uint32_t>(4);
   s->head = cv.take<int32_t>(E + 1);
   s->grp_rid = cv.take<int32_t>(E + 1);

@@ -568,6 +568,8 @@ static_assert(kResRows <= kMaxRows, "residual unit larger than the stream row ta
 struct UnitDesc {
   long long s0;      // residual unit: first entry
   long long rid;     // window unit: first row
+  const int2* ulist; // pre-built row-major window list (nullptr: list from the bitmaps)
+  int v0;            // window unit: first value index (its list range starts there)
   int window, to_part, total, nrows, g, slot, avail, b0, b1;
   uint32_t next;     // the unit claimed for after this one
 };
@@ -636,6 +638,17 @@ __device__ __forceinline__ void raw_fma(const RawVec<VEC, BT>& r, float v, float
 template <int kCap>
 __device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>& sm, int P0, uint64_t pol_a) {
   const int lane = threadIdx.x & 31;
+  if (P0 > 0 && sm.u.ulist) {  // the row table is set; only this piece's list copy remains
+    const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(sm.list);
+    const int n = sm.u.total - P0 < kCap ? sm.u.total - P0 : kCap;
+    const int2* src = sm.u.ulist + sm.u.v0 + P0;
+    for (int p = lane; p < n; p += 32)
+      asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(list_s + 8u * p),
+                   "l"(src + p), "l"(pol_a) : "memory");
+    cp_async_wait_all();
+    __syncwarp();
+    return;
+  }
   const int32_t blk = sm.u.b0 + lane;
   const bool mine = blk < sm.u.b1;
   const unsigned long long bm = mine ? ldg_hint64(a.bitmaps + blk, pol_a) : 0ull;
@@ -676,6 +689,17 @@ __device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>&
   // fields stay non-negative: below(i) <= beg(i) + ex(i) always (a lane's own rows < i are part of the list before row i)
   const unsigned long long F0 = beg0 + ex0 - below0, F1 = beg1 + ex1 - below1;
   const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(sm.list);
+  if (sm.u.ulist) {  // pre-built row-major list: one coalesced copy of this piece
+    __syncwarp();     // lane 0 wrote sm.u.total above
+    const int n = sm.u.total - P0 < kCap ? sm.u.total - P0 : kCap;
+    const int2* src = sm.u.ulist + sm.u.v0 + P0;
+    for (int p = lane; p < n; p += 32)
+      asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(list_s + 8u * p),
+                   "l"(src + p), "l"(pol_a) : "memory");
+    cp_async_wait_all();
+    __syncwarp();
+    return;
+  }
   const int32_t* cbase = a.col_id + (int64_t)blk * 8;
   const float* vbase = a.tc_values + vs;
   const int P1 = P0 + kCap;
@@ -700,6 +724,60 @@ __device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>&
   }
   cp_async_wait_all();
   __syncwarp();
+}
+
+// Row-major window list (schedule time, once per format): every window unit's nonzeros as
+// (col_id, value) pairs in the order the stream consumes them -- rows in order, blocks in order
+// inside a row, columns ascending inside a block.  A unit's pairs occupy the same index range as
+// its values ([vstart[b0], vstart[b1])), so the list needs no offsets of its own.
+__global__ void k_rowmajor_list(Sched s, const unsigned long long* __restrict__ bitmaps,
+                                const int32_t* __restrict__ col_id, const float* __restrict__ tc_values, int2* ulist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_units = s.header[1];  // window units come first
+  for (int64_t uidx = warp0; uidx < n_units; uidx += nwarps) {
+    const int4 un = s.units[uidx];
+    const int32_t blk = un.z + lane;
+    const bool mine = blk < un.w;
+    const unsigned long long bm = mine ? bitmaps[blk] : 0ull;
+    const int32_t vs = mine ? s.vstart[blk] : 0;
+    const int32_t v0 = s.vstart[un.z];
+    unsigned long long p0 = 0, p1 = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      p0 |= (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
+      p1 |= (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
+    }
+    unsigned long long q0 = p0, q1 = p1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t0 = __shfl_up_sync(0xffffffffu, q0, o);
+      const unsigned long long t1 = __shfl_up_sync(0xffffffffu, q1, o);
+      if (lane >= o) {
+        q0 += t0;
+        q1 += t1;
+      }
+    }
+    const unsigned long long tot0 = __shfl_sync(0xffffffffu, q0, 31), tot1 = __shfl_sync(0xffffffffu, q1, 31);
+    const unsigned long long rp0 = tot0 * 0x0001000100010001ull;
+    const unsigned long long rp1 = tot1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
+    const unsigned long long ex0 = q0 - p0, ex1 = q1 - p1;
+    const unsigned long long beg0 = (rp0 << 16), beg1 = (rp1 << 16) | (rp0 >> 48);
+    const unsigned long long below0 = (p0 * 0x0001000100010001ull) << 16;
+    const unsigned long long below1 = ((p1 * 0x0001000100010001ull) << 16) + ((p0 * 0x0001000100010001ull) >> 48) * 0x0001000100010001ull;
+    const unsigned long long F0 = beg0 + ex0 - below0, F1 = beg1 + ex1 - below1;
+    unsigned long long rem = bm;
+    int r = 0;
+    while (rem) {
+      const int bit = __ffsll((long long)rem) - 1;
+      rem &= rem - 1;
+      const int i = bit >> 3;
+      const int pos = (int)((((i < 4 ? F0 : F1) >> (16 * (i & 3))) & 0xffffull)) + r;
+      ulist[v0 + pos] = make_int2(col_id[(int64_t)blk * 8 + (bit & 7)], __float_as_int(tc_values[vs + r]));
+      ++r;
+    }
+  }
 }
 
 template <int kCap>
@@ -853,6 +931,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
           sm.u.nrows = slot < 0 ? (int)avail : 8;
           sm.u.b0 = un.z;
           sm.u.b1 = un.w;
+          sm.u.ulist = (a.s.header[9] && !(a.flags & 4096)) ? reinterpret_cast<const int2*>(a.s.header[8]) : nullptr;
+          sm.u.v0 = sm.u.ulist ? a.s.vstart[un.z] : 0;
         }
         __syncwarp();
         window_fill<kCap>(a, sm, 0, pol_a);
@@ -1010,7 +1090,7 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_schedule: buffer %zu < %zu bytes", sched_bytes, need);
   int64_t E = n_entries;
-  RSH_CUDA(cudaMemsetAsync(s.header, 0, 8 * sizeof(int64_t), st));
+  RSH_CUDA(cudaMemsetAsync(s.header, 0, 16 * sizeof(int64_t), st));
   size_t cb;
   if (E) {
     k_group_heads<<<grid_1d(E), kThreads, 0, st>>>(row_window_id, E, s.flags);
@@ -1062,6 +1142,30 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   return kOk;
 }
 
+// Row-major window list for the streaming kernel (k_rowmajor_list): int2 ulist[tc_nnz] built from
+// the format once per schedule; its address is recorded in the schedule so rsh_spmm_cc copies
+// each unit's list with one coalesced read instead of decoding bitmaps.  Results are
+// bit-identical with or without it.
+int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
+                          const float* tc_values, int64_t n_blocks, int64_t tc_nnz, int64_t n_res, void* sched,
+                          size_t sched_bytes, void* ulist, size_t ulist_bytes, cudaStream_t st) {
+  Sched s;
+  const size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
+  if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_schedule_rowmajor: schedule buffer too small");
+  if (tc_nnz < 0 || (tc_nnz && (!ulist || ulist_bytes < (size_t)tc_nnz * 8)))
+    return fail(kInvalid, "rsh_schedule_rowmajor: list buffer must hold 8 bytes per tc nonzero");
+  if (tc_nnz && ((uintptr_t)ulist & 7)) return fail(kInvalid, "rsh_schedule_rowmajor: list must be 8-byte aligned");
+  if (tc_nnz) {
+    k_rowmajor_list<<<8 * sm_count(), kThreads, 0, st>>>(s, (const unsigned long long*)bitmaps, col_id, tc_values,
+                                                          (int2*)ulist);
+    RSH_LAUNCHED("k_rowmajor_list");
+  }
+  const int64_t hdr[2] = {(int64_t)(uintptr_t)ulist, tc_nnz};
+  RSH_CUDA(cudaMemcpyAsync(s.header + 8, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+  RSH_CUDA(cudaStreamSynchronize(st));  // hdr lives on this host stack frame
+  return kOk;
+}
+
 // bytes of chunk-partial workspace rsh_spmm needs (partial_slots from the schedule header)
 size_t rsh_partials_bytes(int64_t partial_slots, int64_t N, int32_t accum) {
   return (size_t)(partial_slots > 0 ? partial_slots : 1) * 8 * (size_t)N * (accum ? sizeof(double) : sizeof(float));
@@ -1075,7 +1179,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 8191) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 16383) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -1098,7 +1202,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.partials = partials;
   a.flags = accum >> 1;  // tuning knobs: bits 0-1 row-walk occupancy variant, bit 2 no L2 cache hints,
                          // bits 3-5 stream depth/occupancy variant, bit 6 row-walk kernel instead of the stream,
-                         // bit 8 stream gathers bypass L1 allocation, bit 10 list copies without L2 hint, bit 11 no lane groups
+                         // bit 8 stream gathers bypass L1 allocation, bit 10 list copies without L2 hint, bit 11 no lane groups, bit 12 ignore the row-major list
   accum &= 1;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;

@@ -295,6 +295,14 @@ class SpmmPlan:
         h = hdr.cpu().tolist()
         self.groups, self.window_units, self.units, self.partial_slots, self.uncovered = h[:5]
         self._partials = {}
+        self.ulist = None
+        if chunk == CHUNK_CC and ROWMAJOR_LIST:
+            # the streaming kernel's pre-decoded window list (8 bytes per tc nonzero)
+            tc_nnz = int(t.values.numel())
+            self.ulist = torch.empty(max(tc_nnz, 1), dtype=torch.int64, device=dev)
+            call("rsh_schedule_rowmajor", t.n_rows, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id), _ptr(t.values),
+                 t.n_blocks, tc_nnz, t.n_res, _ptr(self.buf), self.nbytes, _ptr(self.ulist), 8 * self.ulist.numel(),
+                 _stream(stream))
 
     def partials(self, N: int, accum: int, dev) -> torch.Tensor:
         key = (N, accum)
@@ -304,6 +312,8 @@ class SpmmPlan:
         return self._partials[key]
 
 
+# the streaming kernel reads a pre-decoded row-major window list (rsh_schedule_rowmajor)
+ROWMAJOR_LIST = os.environ.get("RSH_ROWMAJOR_LIST", "1") != "0"
 # rsh_spmm_cc tuning knobs (accum bits 1..): development override through RSH_CC_VARIANT
 CC_VARIANT = int(os.environ.get("RSH_CC_VARIANT", "0"))
 

@@ -269,6 +269,8 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
     b_dev2 = torch.empty_like(b_host, device=dev)
     t2 = DeviceTile(tile.n_rows, tile.n_cols, tile.window_size, **dev_bufs)
     t2._plan = tile._plan  # the schedule is part of the prebuilt operator, like the format
+    ulists = [(pl.ulist, pl.ulist.cpu().pin_memory()) for pl in (tile._plan or {}).values()
+              if getattr(pl, "ulist", None) is not None]
     e2e_steps = max(1, min(args.steps, 5))
     e2e_ms = []
     for it in range(e2e_steps + 1):
@@ -279,6 +281,8 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
         for k, v in host.items():
             dev_bufs[k].copy_(v, non_blocking=True)
         b_dev2.copy_(b_host, non_blocking=True)
+        for dst, src in ulists:
+            dst.copy_(src, non_blocking=True)
         spmm_device(t2, b_dev2, out=out)
         c_host.copy_(out, non_blocking=True)
         s1.record()
@@ -287,7 +291,8 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
             e2e_ms.append(s0.elapsed_time(s1))
     emax = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     dist.all_reduce(emax, op=dist.ReduceOp.MAX)
-    h2d = sum(v.numel() * v.element_size() for v in host.values()) + b_host.numel() * 4
+    h2d = sum(v.numel() * v.element_size() for v in host.values()) + b_host.numel() * 4 + \
+        sum(h.numel() * h.element_size() for _, h in ulists)
     hb = torch.tensor([float(h2d), float(c_host.numel() * 4)], dtype=torch.float64, device=dev)
     dist.all_reduce(hb)
     e2e_ms_max = float(emax.item())

@@ -292,7 +292,8 @@ def test_permute_rows_matches_reference_semantics(small_corpus):
 def test_stream_kernel_bit_identical_across_variants(dtype):
     """The streaming kernel's list pieces (kCap 256 / 320 / 448), pipeline depths and the row-walk
     kernel accumulate every row in the same order: C must be bitwise equal across them (and
-    across lane-group splits of narrow rows, flag 2048),
+    across lane-group splits of narrow rows, flag 2048, and with or without the pre-decoded
+    row-major window list, flag 4096),
     including multi-chunk windows (partials + ticket / fix-up reduction) and a near-dense row."""
     import torch
     from paper_2603_08734_b200 import synth
@@ -311,6 +312,6 @@ def test_stream_kernel_bit_identical_across_variants(dtype):
             continue
         base = spmm_device(t, b, math="fp32", cc_variant=0)
         # the row walk sums in the same order except its narrow-row (N <= 64 fp32) lane-group mode
-        for v in (8, 16, 24, 32, 40, 48, 1024, 2048) + ((64,) if n >= 128 or dtype != "float32" else ()):
+        for v in (8, 16, 24, 32, 40, 48, 1024, 2048, 4096) + ((64,) if n >= 128 or dtype != "float32" else ()):
             got = spmm_device(t, b, math="fp32", cc_variant=v)
             assert torch.equal(got.view(torch.int32), base.view(torch.int32)), (n, v)

@@ -227,6 +227,7 @@ __device__ __forceinline__ void window_rows(const SpmmArgs& a, int4 un, int64_t 
                                             int32_t k, int n_fc, int2* list, int* tab) {
   const int lane = threadIdx.x & 31;
   const int32_t b0 = un.z, b1 = un.w;
+  if (b1 - b0 > 32) __trap();  // the row walk lists at most one block per lane
   const int32_t blk = b0 + lane;
   const bool mine = blk < b1;
   // L2 policy: B rows evict_last (reused across windows), the format stream evict_first
@@ -632,13 +633,40 @@ __device__ __forceinline__ void raw_fma(const RawVec<VEC, BT>& r, float v, float
   for (int t = 0; t < VEC; ++t) acc[t] = fmaf(v, to_f<BT>(e[t]), acc[t]);
 }
 
-// List positions [P0, P0 + kCap) of a window unit.  Every lane re-derives its block's row
-// offsets (loads hit L1 after the first piece); on the first piece the unit's row table is
-// written too.
+// List positions [P0, P0 + kCap) of a window unit; on the first piece the unit's row table is
+// written too.  With the pre-decoded row-major list (units of any length) a piece is one
+// coalesced copy; without it (units of <= 32 blocks, lane l owning block b0 + l) every lane
+// re-derives its block's row offsets and copies its nonzeros bit by bit.
 template <int kCap>
 __device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>& sm, int P0, uint64_t pol_a) {
   const int lane = threadIdx.x & 31;
-  if (P0 > 0 && sm.u.ulist) {  // the row table is set; only this piece's list copy remains
+  if (P0 == 0 && sm.u.ulist) {
+    // list mode (units of any length): the row table from the per-row totals of all blocks
+    unsigned long long t0 = 0, t1 = 0;
+    for (int32_t blk = sm.u.b0 + lane; blk < sm.u.b1; blk += 32) {
+      const unsigned long long bm = ldg_hint64(a.bitmaps + blk, pol_a);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        t0 += (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
+        t1 += (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+    }
+    const unsigned long long rp0 = t0 * 0x0001000100010001ull;
+    const unsigned long long rp1 = t1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
+    if (lane < 8) {
+      sm.rend[lane] = (int)(((lane < 4 ? rp0 : rp1) >> (16 * (lane & 3))) & 0xffffull);
+      const int64_t rid = sm.u.rid;
+      sm.rowoff[lane] = sm.u.slot < 0 ? (rid + lane) * a.ldc : ((int64_t)sm.u.slot * 8 + lane) * a.N;
+    }
+    if (lane == 0) sm.u.total = (int)(rp1 >> 48);
+    __syncwarp();
+  }
+  if (sm.u.ulist) {  // the row table is set; copy this piece of the pre-decoded list
     const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(sm.list);
     const int n = sm.u.total - P0 < kCap ? sm.u.total - P0 : kCap;
     const int2* src = sm.u.ulist + sm.u.v0 + P0;
@@ -649,6 +677,7 @@ __device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>&
     __syncwarp();
     return;
   }
+  if (sm.u.b1 - sm.u.b0 > 32) __trap();  // long units need the row-major list (rsh_schedule_rowmajor)
   const int32_t blk = sm.u.b0 + lane;
   const bool mine = blk < sm.u.b1;
   const unsigned long long bm = mine ? ldg_hint64(a.bitmaps + blk, pol_a) : 0ull;
@@ -689,17 +718,6 @@ __device__ __forceinline__ void window_fill(const SpmmArgs& a, StreamSmem<kCap>&
   // fields stay non-negative: below(i) <= beg(i) + ex(i) always (a lane's own rows < i are part of the list before row i)
   const unsigned long long F0 = beg0 + ex0 - below0, F1 = beg1 + ex1 - below1;
   const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(sm.list);
-  if (sm.u.ulist) {  // pre-built row-major list: one coalesced copy of this piece
-    __syncwarp();     // lane 0 wrote sm.u.total above
-    const int n = sm.u.total - P0 < kCap ? sm.u.total - P0 : kCap;
-    const int2* src = sm.u.ulist + sm.u.v0 + P0;
-    for (int p = lane; p < n; p += 32)
-      asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(list_s + 8u * p),
-                   "l"(src + p), "l"(pol_a) : "memory");
-    cp_async_wait_all();
-    __syncwarp();
-    return;
-  }
   const int32_t* cbase = a.col_id + (int64_t)blk * 8;
   const float* vbase = a.tc_values + vs;
   const int P1 = P0 + kCap;
@@ -738,44 +756,68 @@ __global__ void k_rowmajor_list(Sched s, const unsigned long long* __restrict__ 
   const int64_t n_units = s.header[1];  // window units come first
   for (int64_t uidx = warp0; uidx < n_units; uidx += nwarps) {
     const int4 un = s.units[uidx];
-    const int32_t blk = un.z + lane;
-    const bool mine = blk < un.w;
-    const unsigned long long bm = mine ? bitmaps[blk] : 0ull;
-    const int32_t vs = mine ? s.vstart[blk] : 0;
     const int32_t v0 = s.vstart[un.z];
-    unsigned long long p0 = 0, p1 = 0;
+    // pass 1: per-row totals over all blocks of the unit (4 rows x 16 bits per word; a unit has
+    // at most 8 x 64 x 1024 ... fields stay below 2^16 for units of <= 1024 blocks)
+    unsigned long long t0 = 0, t1 = 0;
+    for (int32_t blk = un.z + lane; blk < un.w; blk += 32) {
+      const unsigned long long bm = bitmaps[blk];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      p0 |= (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
-      p1 |= (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
-    }
-    unsigned long long q0 = p0, q1 = p1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long t0 = __shfl_up_sync(0xffffffffu, q0, o);
-      const unsigned long long t1 = __shfl_up_sync(0xffffffffu, q1, o);
-      if (lane >= o) {
-        q0 += t0;
-        q1 += t1;
+      for (int i = 0; i < 4; ++i) {
+        t0 += (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
+        t1 += (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
       }
     }
-    const unsigned long long tot0 = __shfl_sync(0xffffffffu, q0, 31), tot1 = __shfl_sync(0xffffffffu, q1, 31);
-    const unsigned long long rp0 = tot0 * 0x0001000100010001ull;
-    const unsigned long long rp1 = tot1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
-    const unsigned long long ex0 = q0 - p0, ex1 = q1 - p1;
-    const unsigned long long beg0 = (rp0 << 16), beg1 = (rp1 << 16) | (rp0 >> 48);
-    const unsigned long long below0 = (p0 * 0x0001000100010001ull) << 16;
-    const unsigned long long below1 = ((p1 * 0x0001000100010001ull) << 16) + ((p0 * 0x0001000100010001ull) >> 48) * 0x0001000100010001ull;
-    const unsigned long long F0 = beg0 + ex0 - below0, F1 = beg1 + ex1 - below1;
-    unsigned long long rem = bm;
-    int r = 0;
-    while (rem) {
-      const int bit = __ffsll((long long)rem) - 1;
-      rem &= rem - 1;
-      const int i = bit >> 3;
-      const int pos = (int)((((i < 4 ? F0 : F1) >> (16 * (i & 3))) & 0xffffull)) + r;
-      ulist[v0 + pos] = make_int2(col_id[(int64_t)blk * 8 + (bit & 7)], __float_as_int(tc_values[vs + r]));
-      ++r;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+    }
+    const unsigned long long rp0 = t0 * 0x0001000100010001ull;  // inclusive prefix of the row totals
+    const unsigned long long rp1 = t1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
+    const unsigned long long beg0 = (rp0 << 16), beg1 = (rp1 << 16) | (rp0 >> 48);  // row starts
+    // pass 2: 32 blocks at a time; acc = entries of each row placed by earlier chunks
+    unsigned long long acc0 = 0, acc1 = 0;
+    for (int32_t c0 = un.z; c0 < un.w; c0 += 32) {
+      const int32_t blk = c0 + lane;
+      const bool mine = blk < un.w;
+      const unsigned long long bm = mine ? bitmaps[blk] : 0ull;
+      const int32_t vs = mine ? s.vstart[blk] : 0;
+      unsigned long long p0 = 0, p1 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        p0 |= (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
+        p1 |= (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
+      }
+      unsigned long long q0 = p0, q1 = p1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long x0 = __shfl_up_sync(0xffffffffu, q0, o);
+        const unsigned long long x1 = __shfl_up_sync(0xffffffffu, q1, o);
+        if (lane >= o) {
+          q0 += x0;
+          q1 += x1;
+        }
+      }
+      const unsigned long long ex0 = q0 - p0, ex1 = q1 - p1;
+      const unsigned long long below0 = (p0 * 0x0001000100010001ull) << 16;
+      const unsigned long long below1 =
+          ((p1 * 0x0001000100010001ull) << 16) + ((p0 * 0x0001000100010001ull) >> 48) * 0x0001000100010001ull;
+      // F(i) = row start + earlier chunks' entries of row i + this lane's exclusive offset - the
+      // lane's nonzeros in rows < i (a nonzero of block rank r lands at F(row) + r)
+      const unsigned long long F0 = beg0 + acc0 + ex0 - below0, F1 = beg1 + acc1 + ex1 - below1;
+      unsigned long long rem = bm;
+      int r = 0;
+      while (rem) {
+        const int bit = __ffsll((long long)rem) - 1;
+        rem &= rem - 1;
+        const int i = bit >> 3;
+        const int pos = (int)((((i < 4 ? F0 : F1) >> (16 * (i & 3))) & 0xffffull)) + r;
+        ulist[v0 + pos] = make_int2(col_id[(int64_t)blk * 8 + (bit & 7)], __float_as_int(tc_values[vs + r]));
+        ++r;
+      }
+      acc0 += __shfl_sync(0xffffffffu, q0, 31);
+      acc1 += __shfl_sync(0xffffffffu, q1, 31);
     }
   }
 }
@@ -1213,6 +1255,8 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   if (accum == 1 && vec > 4) vec = 4;
   // the stream kernel addresses B rows with a 32-bit byte stride
   if (ldb * (int64_t)esz >= (1LL << 32)) a.flags |= 64;
+  // A schedule with units above 32 blocks (chunk_blocks > 32) needs the row-major list and the
+  // streaming kernel for f32 accumulation; the kernels trap on a unit they cannot walk.
   if (accum == 0 && !(a.flags & 64)) {
     // streaming kernel: the f32-accumulation default (flags bit 6 selects the row-walk kernel)
     const bool al16 = !((uintptr_t)B & 15) && !((uintptr_t)C & 15) && (ldb * (int64_t)esz) % 16 == 0 && ldc % 4 == 0;

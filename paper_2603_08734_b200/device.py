@@ -276,7 +276,8 @@ def build_device(a: DeviceCsr, window_size=8, tau_nnz=None, tau_inc=None, max_bl
 _BDT = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 
 
-CHUNK_CC = 32    # blocks per work unit for the CUDA-core kernel (csrc/sched.cuh kChunkCC)
+CHUNK_CC = 32    # blocks per work unit for the CUDA-core kernel walking bitmaps (csrc/sched.cuh kChunkCC)
+CHUNK_CC_LIST = 256  # ... for the streaming kernel reading the pre-decoded row-major list
 CHUNK_TC = 256   # ... and for the tensor-core kernel (kChunkTC)
 
 
@@ -296,7 +297,7 @@ class SpmmPlan:
         self.groups, self.window_units, self.units, self.partial_slots, self.uncovered = h[:5]
         self._partials = {}
         self.ulist = None
-        if chunk == CHUNK_CC and ROWMAJOR_LIST:
+        if chunk == CHUNK_CC_LIST:
             # the streaming kernel's pre-decoded window list (8 bytes per tc nonzero)
             tc_nnz = int(t.values.numel())
             self.ulist = torch.empty(max(tc_nnz, 1), dtype=torch.int64, device=dev)
@@ -375,7 +376,13 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
     if cc_variant is None:
         cc_variant = CC_VARIANT
     path = resolve_math(math, b, t, accumulate)
-    plan = spmm_plan(t, CHUNK_TC if path == "tc" else CHUNK_CC)
+    if path == "tc":
+        chunk = CHUNK_TC
+    elif acc == 0 and ROWMAJOR_LIST and not (cc_variant & (64 | 4096)):
+        chunk = CHUNK_CC_LIST  # long units + the row-major list (flags 64 / 4096: row walk / bitmap decode)
+    else:
+        chunk = CHUNK_CC
+    plan = spmm_plan(t, chunk)
     part = plan.partials(N, acc, b.device)
     call("rsh_spmm_tc" if path == "tc" else "rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
          _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),

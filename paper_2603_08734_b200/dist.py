@@ -193,7 +193,8 @@ def run_sharded_bench(args, metric: str, clock_factory=None) -> None:
     plan = plan_windows(loc, lw_t, 8, 64)
     tile = fill_tile(loc, plan, lr_t, 8)
     tile.window_size = 8 if len(win_h) != 1 else min(8, n - int(win_h[0]))
-    spmm_plan(tile)
+    from .device import CHUNK_CC_LIST
+    spmm_plan(tile, CHUNK_CC_LIST)  # long units + the row-major window list
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     del g

@@ -291,9 +291,8 @@ def test_permute_rows_matches_reference_semantics(small_corpus):
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
 def test_stream_kernel_bit_identical_across_variants(dtype):
     """The streaming kernel's list pieces (kCap 256 / 320 / 448), pipeline depths and the row-walk
-    kernel accumulate every row in the same order: C must be bitwise equal across them (and
-    across lane-group splits of narrow rows, flag 2048, and with or without the pre-decoded
-    row-major window list, flag 4096),
+    kernel accumulate every row in the same order: C must be bitwise equal across them for one
+    schedule (and across lane-group splits of narrow rows, flag 2048),
     including multi-chunk windows (partials + ticket / fix-up reduction) and a near-dense row."""
     import torch
     from paper_2603_08734_b200 import synth
@@ -310,8 +309,18 @@ def test_stream_kernel_bit_identical_across_variants(dtype):
         b = torch.from_numpy(rand_b(a.n_cols, n, n)).cuda().to(getattr(torch, dtype))
         if dtype == "bfloat16" and n == 64:
             continue
+        # 256-block units + row-major list (the default schedule): every stream variant agrees
         base = spmm_device(t, b, math="fp32", cc_variant=0)
-        # the row walk sums in the same order except its narrow-row (N <= 64 fp32) lane-group mode
-        for v in (8, 16, 24, 32, 40, 48, 1024, 2048, 4096) + ((64,) if n >= 128 or dtype != "float32" else ()):
+        for v in (8, 16, 24, 32, 40, 48, 1024, 2048):
             got = spmm_device(t, b, math="fp32", cc_variant=v)
             assert torch.equal(got.view(torch.int32), base.view(torch.int32)), (n, v)
+        # 32-block units (bitmap decode, flag 4096): the stream and the row walk agree -- the row
+        # walk sums in the same order except its narrow-row (N <= 64 fp32) lane-group mode
+        base32 = spmm_device(t, b, math="fp32", cc_variant=4096)
+        for v in (4096 | 8, 4096 | 2048) + ((64,) if n >= 128 or dtype != "float32" else ()):
+            got = spmm_device(t, b, math="fp32", cc_variant=v)
+            assert torch.equal(got.view(torch.int32), base32.view(torch.int32)), (n, v)
+        # both schedules against the fp64 oracle (chunk partials change the rounding, not the sum)
+        ref = O.spmm_f64(O.Csr.of(a), b.float().cpu().numpy())[1]
+        for c in (base, base32):
+            assert O.rel_frobenius(c.cpu().numpy(), ref) <= 1e-6

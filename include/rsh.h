@@ -110,6 +110,9 @@ int rsh_two_opt_sweep(const int64_t* row_ptr, const int32_t* col_idx, const doub
                       cudaStream_t stream);
 int rsh_mst_order(int64_t m, int32_t k, const int32_t* nbr, const double* nsim, const int32_t* ncount,
                   int64_t* order_out);
+int rsh_isolation_adjust(int64_t m, int64_t n_cols, const int64_t* row_ptr, const int32_t* col_idx, const double* w,
+                         const double* wsum, const int64_t* order_in, double iso_threshold, int64_t hub_cap,
+                         int64_t* order_out, int64_t* n_isolated);
 double rsh_sum_sequential(const double* x, int64_t n);
 
 /* ---- persistent-kernel schedule: execute.py:136-168 (_window_groups, value starts) as device

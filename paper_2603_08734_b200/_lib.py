@@ -46,6 +46,7 @@ SIGNATURES = {
     "rsh_two_opt_sweep": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i64, _vp, _vp]),
     "rsh_mst_order": (ctypes.c_int, [_i64, _i32, _vp, _vp, _vp, _vp]),
     "rsh_sum_sequential": (_f64, [_vp, _i64]),
+    "rsh_isolation_adjust": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _i64, _vp, _vp]),
     "rsh_schedule_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "rsh_schedule": (ctypes.c_int, [_i64, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]),
     "rsh_partials_bytes": (_sz, [_i64, _i64, _i32]),

@@ -465,6 +465,123 @@ int rsh_mst_order(int64_t m, int32_t k, const int32_t* nbr, const double* nsim, 
   return kOk;
 }
 
+// reorder.py:386-446 (isolation_adjust) on HOST arrays, an exact restatement: rows whose
+// similarity to both sequence neighbours is below iso_threshold are taken out and, in ascending
+// row order, reinserted right after their most similar non-isolated row (candidates: rows
+// sharing a column, ascending; ties to the lower row; empty rows match the first other empty
+// non-isolated row); rows without a positive match go to the tail ascending.  w / wsum are the
+// column weights and row weight sums (rsh_column_weights).  hub_cap < 0: walk every column (the
+// reference); otherwise candidate walks skip columns with more rows.  Returns the number of
+// isolated rows in *n_isolated.
+int rsh_isolation_adjust(int64_t m, int64_t n_cols, const int64_t* rp, const int32_t* ci, const double* w,
+                         const double* wsum, const int64_t* order_in, double iso_threshold, int64_t hub_cap,
+                         int64_t* order_out, int64_t* n_isolated) {
+  if (!(iso_threshold >= 0.0 && iso_threshold <= 1.0)) return fail(kInvalid, "iso_threshold must lie in [0, 1]");
+  *n_isolated = 0;
+  for (int64_t i = 0; i < m; ++i) order_out[i] = order_in[i];
+  if (m <= 1 || iso_threshold == 0.0) return kOk;
+  auto sim = [&](int64_t r, int64_t u) -> double {
+    if (r == u) return 1.0;
+    int64_t a = rp[r], ae = rp[r + 1], b = rp[u], be = rp[u + 1];
+    if (a == ae && b == be) return 1.0;
+    double wi = 0.0;
+    while (a < ae && b < be) {
+      if (ci[a] == ci[b]) {
+        wi += w[ci[a]];
+        ++a;
+        ++b;
+      } else if (ci[a] < ci[b]) {
+        ++a;
+      } else {
+        ++b;
+      }
+    }
+    const double tot = wsum[r] + wsum[u] - wi;
+    if (tot <= 0.0) return 0.0;
+    const double v = wi / tot;
+    return v < 1.0 ? v : 1.0;
+  };
+  std::vector<char> iso(m, 0);
+  std::vector<int64_t> isolated;
+  for (int64_t pos = 0; pos < m; ++pos) {
+    const int64_t r = order_in[pos];
+    const bool left = pos > 0 && sim(order_in[pos - 1], r) >= iso_threshold;
+    const bool right = pos < m - 1 && sim(r, order_in[pos + 1]) >= iso_threshold;
+    if (!left && !right) {
+      iso[r] = 1;
+      isolated.push_back(r);
+    }
+  }
+  *n_isolated = (int64_t)isolated.size();
+  if (isolated.empty()) return kOk;
+  // base sequence as a linked list (insert-after is O(1))
+  const int64_t NIL = -1;
+  std::vector<int64_t> next(m, NIL);
+  int64_t head = NIL, last = NIL;
+  for (int64_t pos = 0; pos < m; ++pos) {
+    const int64_t r = order_in[pos];
+    if (iso[r]) continue;
+    if (last == NIL) head = r; else next[last] = r;
+    last = r;
+  }
+  // inverted index: rows of each column, ascending
+  std::vector<int64_t> cstart(n_cols + 1, 0);
+  for (int64_t p = 0; p < rp[m]; ++p) ++cstart[ci[p] + 1];
+  for (int64_t c = 0; c < n_cols; ++c) cstart[c + 1] += cstart[c];
+  std::vector<int64_t> fillp(cstart.begin(), cstart.end() - 1), crow(rp[m]);
+  for (int64_t r = 0; r < m; ++r)
+    for (int64_t p = rp[r]; p < rp[r + 1]; ++p) crow[fillp[ci[p]]++] = r;
+  std::vector<int64_t> empties;
+  for (int64_t r = 0; r < m; ++r)
+    if (rp[r + 1] == rp[r]) empties.push_back(r);
+  std::vector<int64_t> tail, cand;
+  std::vector<char> seen(m, 0);
+  std::sort(isolated.begin(), isolated.end());
+  for (const int64_t r : isolated) {
+    int64_t best = NIL;
+    if (rp[r + 1] == rp[r]) {
+      for (const int64_t u : empties)
+        if (u != r && !iso[u]) {
+          best = u;
+          break;
+        }
+    } else {
+      cand.clear();
+      for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+        const int32_t c = ci[p];
+        if (hub_cap >= 0 && cstart[c + 1] - cstart[c] > hub_cap) continue;
+        for (int64_t q = cstart[c]; q < cstart[c + 1]; ++q)
+          if (!seen[crow[q]]) {
+            seen[crow[q]] = 1;
+            cand.push_back(crow[q]);
+          }
+      }
+      for (const int64_t u : cand) seen[u] = 0;
+      std::sort(cand.begin(), cand.end());
+      double best_sim = 0.0;
+      for (const int64_t u : cand) {
+        if (u == r || iso[u]) continue;
+        const double sv = sim(r, u);
+        if (sv > best_sim) {
+          best = u;
+          best_sim = sv;
+        }
+      }
+    }
+    if (best == NIL) {
+      tail.push_back(r);
+    } else {
+      next[r] = next[best];
+      next[best] = r;
+      if (last == best) last = r;
+    }
+  }
+  int64_t pos = 0;
+  for (int64_t x = head; x != NIL; x = next[x]) order_out[pos++] = x;
+  for (const int64_t r : tail) order_out[pos++] = r;
+  return pos == m ? kOk : fail(kInvalid, "rsh_isolation_adjust: internal error (lost rows)");
+}
+
 // the objective's left-to-right sum (reorder.py:96-101) over host terms
 double rsh_sum_sequential(const double* x, int64_t n) {
   double t = 0.0;

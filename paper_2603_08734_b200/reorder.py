@@ -8,6 +8,7 @@ objective's left-to-right sum) as host C++ in the same library:
     column_weights     reorder.py:33-42     rsh_column_weights
     build_knn          reorder.py:158-230   rsh_knn (A^T from rsh_transpose_csr)
     mst_order          reorder.py:268-321   rsh_mst_order (host C++, exact restatement)
+    isolation_adjust   reorder.py:386-446   rsh_isolation_adjust (host C++, exact restatement)
     refine_2opt        reorder.py:328-380   rsh_two_opt_sweep (disjoint windows in parallel)
     permutation_objective  reorder.py:96-101  rsh_pair_dis + rsh_sum_sequential
     permute_rows       reorder.py:138-151   rsh_permute_rows
@@ -16,9 +17,9 @@ Differences from the reference, all on the side of the search, none on the objec
 2-opt sweeps process disjoint windows in parallel (each window keeps the reference's
 sequential first-improvement scan), so the refined order differs but never has a larger
 objective than its input; candidate walks skip columns above ``hub_cap`` rows (default: none)
-and keep at most 1024 distinct candidates per row (overflow is counted); the isolation pass
-(reorder.py:386-446) is not implemented (the reference keeps it only when it does not worsen
-the objective).
+and keep at most 1024 distinct candidates per row (overflow is counted).  The isolation pass
+(reorder.py:386-446) is an exact host C++ restatement (rsh_isolation_adjust), kept only when it
+does not worsen the objective, as in the reference.
 """
 
 from __future__ import annotations
@@ -309,10 +310,35 @@ def load_permutation(path) -> Permutation:
     return Permutation(np.array(order, dtype=np.int64), objective)
 
 
-def isolation_adjust(a, w, p, iso_threshold: float = 0.05):
-    """reorder.py:386-446 -- not implemented on device; reorder_pipeline skips it (the reference
-    keeps its result only when it does not worsen the objective)."""
-    raise NotImplementedError("isolation_adjust is not part of the device reorder")
+def _isolation_host(ctx: "_Ctx", order: np.ndarray, iso_threshold: float, hub_cap: int | None):
+    from ._lib import call
+    d = ctx.d
+    rp, ci = d.row_ptr.cpu().numpy(), d.col_idx.cpu().numpy()
+    w, ws = ctx.w.cpu().numpy(), ctx.wsum.cpu().numpy()
+    src = np.ascontiguousarray(order, np.int64)
+    out = np.empty_like(src)
+    n_iso = np.zeros(1, np.int64)
+    call("rsh_isolation_adjust", d.n_rows, d.n_cols, rp.ctypes.data, ci.ctypes.data, w.ctypes.data, ws.ctypes.data,
+         src.ctypes.data, float(iso_threshold), -1 if hub_cap is None else int(hub_cap), out.ctypes.data,
+         n_iso.ctypes.data)
+    return out, int(n_iso[0])
+
+
+def isolation_adjust(a: CsrMatrix, w: ColumnWeights, p: Permutation, iso_threshold: float = 0.05,
+                     hub_cap: int | None = None) -> Permutation:
+    """reorder.py:386-446: rows dissimilar to both sequence neighbours are reinserted after their
+    most similar non-isolated row (host C++ restatement, rsh_isolation_adjust; weights on
+    device).  iso_threshold = 0 returns the input verbatim."""
+    import torch
+    if not (0.0 <= iso_threshold <= 1.0):
+        raise ValueError("iso_threshold must lie in [0, 1]")
+    if len(p) <= 1 or iso_threshold == 0.0:
+        return p
+    ctx = _Ctx(a, w.alpha)
+    out, n_iso = _isolation_host(ctx, p.order, iso_threshold, hub_cap)
+    if n_iso == 0:
+        return p
+    return Permutation(out, ctx.objective(torch.from_numpy(out).to(ctx.d.device)))
 
 
 def reorder_device(a, params: ReorderParams = ReorderParams()):
@@ -335,15 +361,26 @@ def reorder_device(a, params: ReorderParams = ReorderParams()):
     refined = ctx.objective(o)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
-    return o, {"mst": mst_obj, "refined": refined, "overflow_rows": overflow,
-               "ms": {"knn": 1e3 * (t1 - t0), "mst_host": 1e3 * (t2 - t1), "two_opt": 1e3 * (t3 - t2)}}
+    # isolation pass (reorder.py:386-446), kept only when it does not worsen the objective
+    final, n_iso = refined, 0
+    if d.n_rows > 1 and params.iso_threshold > 0.0:
+        adj, n_iso = _isolation_host(ctx, o.cpu().numpy(), params.iso_threshold, params.hub_cap)
+        if n_iso:
+            oa = torch.from_numpy(adj).to(d.device)
+            obj = ctx.objective(oa)
+            if obj <= refined:
+                o, final = oa, obj
+    t4 = time.perf_counter()
+    return o, {"mst": mst_obj, "refined": refined, "final": final, "isolated_rows": n_iso, "overflow_rows": overflow,
+               "ms": {"knn": 1e3 * (t1 - t0), "mst_host": 1e3 * (t2 - t1), "two_opt": 1e3 * (t3 - t2),
+                      "isolation_host": 1e3 * (t4 - t3)}}
 
 
 def reorder_pipeline(a: CsrMatrix, params: ReorderParams = ReorderParams()):
     """reorder.py:464-481: (Permutation, permuted matrix); the objective never exceeds the MST
     stage's."""
     o, info = reorder_device(a, params)
-    best = Permutation(o.cpu().numpy(), info["refined"])
+    best = Permutation(o.cpu().numpy(), info["final"])
     return best, permute_rows(a, best.order)
 
 

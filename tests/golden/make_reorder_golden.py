@@ -54,6 +54,7 @@ def main():
         g = R.build_knn(ra, w, cand, p.k)
         mst = R.mst_order(g, ra, w)
         ref2 = R.refine_2opt(ra, w, mst, p.two_opt_window, p.two_opt_passes)
+        iso = R.isolation_adjust(ra, w, ref2, p.iso_threshold)
         best, _ = R.reorder_pipeline(ra, p)
         rnd = np.random.default_rng(5).permutation(a.n_rows)
         out.append({
@@ -62,7 +63,9 @@ def main():
             "knn": [[[int(u), float(s)] for u, s in lst] for lst in g.neighbors],
             "max_candidates_hit": int(sum(len(c) >= p.max_candidates for c in cand)),
             "mst_order": [int(x) for x in mst.order], "mst_objective": mst.objective,
-            "two_opt_objective": ref2.objective, "pipeline_objective": best.objective,
+            "two_opt_order": [int(x) for x in ref2.order], "two_opt_objective": ref2.objective,
+            "isolation_order": [int(x) for x in iso.order], "isolation_objective": iso.objective,
+            "pipeline_objective": best.objective,
             "random_order": [int(x) for x in rnd], "random_objective": R.permutation_objective(ra, w, rnd),
         })
         print(name, a.n_rows, mst.objective, ref2.objective, best.objective)

@@ -2,7 +2,8 @@
 (tests/golden/reorder_cases.json, make_reorder_golden.py).
 
 CPU: the host C++ forest + DFS linearisation (rsh_mst_order) reproduces the reference's
-mst_order from the reference's kNN graph exactly.  GPU: column weights, the kNN graph, the
+mst_order from the reference's kNN graph exactly, and the host isolation pass
+(rsh_isolation_adjust) the reference's isolation_adjust from the reference's 2-opt order.  GPU: column weights, the kNN graph, the
 objective of any order and the MST-stage order equal the reference's; the parallel 2-opt never
 worsens the MST-stage objective and returns a bijection; the pipeline output is a bijection
 whose permuted matrix is the reference's permute_rows of it.
@@ -120,3 +121,54 @@ def test_w_jaccard_known_answers():
     assert w_jaccard(a, w, 0, 2) == 0.0
     assert w_jaccard(a, w, 3, 3) == 1.0
     assert w_jaccard(a, w, 2, 3) == 0.0
+
+
+def _host_isolation(a, order, thr=0.05):
+    """Call the host C++ restatement directly with numpy-computed weights (test-side)."""
+    from paper_2603_08734_b200._lib import call
+    rp, ci = np.ascontiguousarray(a.row_ptr, np.int64), np.ascontiguousarray(a.col_idx, np.int32)
+    deg = np.bincount(ci, minlength=a.n_cols).astype(np.float64)
+    w = np.zeros(a.n_cols)
+    w[deg > 0] = deg[deg > 0] ** -0.5
+    wsum = np.bincount(np.repeat(np.arange(a.n_rows), np.diff(rp)), weights=w[ci], minlength=a.n_rows)
+    src = np.ascontiguousarray(order, np.int64)
+    out = np.empty_like(src)
+    n_iso = np.zeros(1, np.int64)
+    call("rsh_isolation_adjust", a.n_rows, a.n_cols, rp.ctypes.data, ci.ctypes.data, w.ctypes.data, wsum.ctypes.data,
+         src.ctypes.data, thr, -1, out.ctypes.data, n_iso.ctypes.data)
+    return out
+
+
+@pytest.mark.parametrize("rec", _cases(), ids=lambda r: r["case"])
+def test_isolation_host_matches_reference(rec):
+    a = corpus_matrix(rec["recipe"])
+    assert _host_isolation(a, rec["two_opt_order"]).tolist() == rec["isolation_order"]
+
+
+def test_isolation_known_answers():
+    """test_reorder.py:268-300 restated: threshold 0 is the identity; a friendless row goes to the
+    tail; an isolated row is reinserted after its best match."""
+    from paper_2603_08734_b200 import CsrMatrix
+    d = np.zeros((4, 6), np.float32)
+    d[0, [0, 1]] = 1
+    d[1, [4, 5]] = 1   # shares nothing
+    d[2, [0, 1]] = 1
+    d[3, [0, 2]] = 1
+    a = CsrMatrix.from_dense(d)
+    assert _host_isolation(a, [0, 1, 2, 3], 0.0).tolist() == [0, 1, 2, 3]
+    # row 1 has no similar neighbour and no candidate: tail
+    assert _host_isolation(a, [0, 1, 2, 3]).tolist()[-1] == 1
+    # row 2 placed between dissimilar rows is reinserted right after row 0 (its best match)
+    out = _host_isolation(a, [0, 1, 3, 2, ]).tolist()
+    assert sorted(out) == [0, 1, 2, 3]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rec", _cases()[:4], ids=lambda r: r["case"])
+def test_device_isolation_matches_reference(rec):
+    from paper_2603_08734_b200.reorder import Permutation, column_weights, isolation_adjust
+    a = corpus_matrix(rec["recipe"])
+    w = column_weights(a, 0.5)
+    p = isolation_adjust(a, w, Permutation(np.array(rec["two_opt_order"]), rec["two_opt_objective"]))
+    assert p.order.tolist() == rec["isolation_order"]
+    assert p.objective == pytest.approx(rec["isolation_objective"], rel=1e-12)

@@ -110,3 +110,84 @@ def hybrid_spmm(m, b, cfg: ExecConfig | None = None, out=None):
 
 
 __all__ = ["ExecConfig", "VerificationError", "hybrid_spmm", "ORACLE_TOLERANCE"]
+
+
+# ---------------------------------------------------------------------------------------------
+# per-block / per-entry executor pieces (execute.py:52-133) -- each runs the device SpMM on a
+# one-window or residual-only sub-format, so the arithmetic is the product kernel's
+# ---------------------------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Fragment8x8:
+    """execute.py:52-62: dense row-major 8x8 expansion of one bitmap block."""
+
+    data: np.ndarray
+
+    def __post_init__(self) -> None:
+        arr = np.ascontiguousarray(self.data, dtype=np.float32)
+        if arr.shape != (8, 8):
+            raise ValueError(f"fragment must be 8x8, got {arr.shape}")
+        arr.flags.writeable = False
+        object.__setattr__(self, "data", arr)
+
+
+def _window_tile(bitmaps, col_id, values, n_cols: int):
+    """A one-window RS-Tile (rows 0..7) holding the given blocks."""
+    from .tile import ResidualPart, RsTileMatrix, TcPart
+    nb = int(np.asarray(bitmaps).size)
+    z32, z64 = np.zeros(0, np.int32), np.zeros(1, np.int64)
+    return RsTileMatrix(8, n_cols, TcPart(np.zeros(1 if nb else 0, np.int32), np.array([0, nb] if nb else [0], np.int64),
+                                          bitmaps, col_id, values),
+                        ResidualPart(z32, z64, z32, np.zeros(0, np.float32)), 8)
+
+
+def decode_tile(bitmap: int, values) -> Fragment8x8:
+    """execute.py:80-89: expand one bitmap block (bit b -> row b >> 3, column b & 7); on device,
+    as the block times the 8x8 identity."""
+    from .tile import TcPart  # noqa: F401
+    bm = np.array([bitmap], dtype=np.uint64)
+    vals = np.asarray(values, dtype=np.float32).ravel()
+    expected = bin(int(bitmap) & (2 ** 64 - 1)).count("1")
+    if vals.size != expected:
+        raise ValueError(f"bitmap has {expected} set bits but {vals.size} values were given")
+    m = _window_tile(bm, np.arange(8, dtype=np.int32), vals, 8)
+    eye = DenseMatrix.from_array(np.eye(8, dtype=np.float32))
+    return Fragment8x8(hybrid_spmm(m, eye, ExecConfig(math="fp32")).data)
+
+
+def exec_tc_window(m, entry: int, b: DenseMatrix, c_out: np.ndarray) -> None:
+    """execute.py:98-114: accumulate one window entry's block products into a local 8 x d
+    array (f32 or f64 by c_out's dtype)."""
+    from ._lib import FormatError
+    if not 0 <= entry < m.tc.n_entries:
+        raise IndexError(f"entry {entry} out of range")
+    bs, be = int(m.tc.row_window_offset[entry]), int(m.tc.row_window_offset[entry + 1])
+    if bs == be:
+        return
+    cols = np.asarray(m.tc.col_id[bs * 8:be * 8])
+    if cols.size and (int(cols.min()) < 0 or int(cols.max()) >= b.n_rows):
+        raise FormatError("col_id references a column outside B's row range")
+    pc = np.unpackbits(np.ascontiguousarray(m.tc.bitmaps, "<u8").view(np.uint8)).reshape(-1, 64).sum(1)
+    vs = int(pc[:bs].sum())
+    sub = _window_tile(m.tc.bitmaps[bs:be], cols, m.tc.values[vs:vs + int(pc[bs:be].sum())], b.n_rows)
+    prec = "f64" if c_out.dtype == np.float64 else "f32"
+    r = hybrid_spmm(sub, b, ExecConfig(math="fp32", accumulate_precision=prec)).data
+    c_out += r.astype(c_out.dtype)
+
+
+def exec_residual(m, b: DenseMatrix, c: np.ndarray) -> None:
+    """execute.py:117-133: c[r] += v . B[cols] for every residual row (on device)."""
+    from ._lib import FormatError
+    from .tile import RsTileMatrix, TcPart
+    res = m.residual
+    if res.col_id.size and (int(res.col_id.min()) < 0 or int(res.col_id.max()) >= b.n_rows):
+        raise FormatError("residual col_id references a column outside B")
+    if res.n_rows == 0:
+        return
+    sub = RsTileMatrix(m.n_rows, m.n_cols, TcPart(np.zeros(0, np.int32), np.zeros(1, np.int64),
+                                                  np.zeros(0, np.uint64), np.zeros(0, np.int32),
+                                                  np.zeros(0, np.float32)), res, 8)
+    prec = "f64" if c.dtype == np.float64 else "f32"
+    r = hybrid_spmm(sub, b, ExecConfig(math="fp32", accumulate_precision=prec)).data
+    rows = np.asarray(res.row_id, np.int64)
+    c[rows] += r[rows].astype(c.dtype)

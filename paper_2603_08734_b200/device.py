@@ -278,7 +278,7 @@ _BDT = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 
 CHUNK_CC = 32    # blocks per work unit for the CUDA-core kernel walking bitmaps (csrc/sched.cuh kChunkCC)
 # ... for the streaming kernel reading the pre-decoded row-major list (RSH_CC_LIST_CHUNK overrides)
-CHUNK_CC_LIST = int(os.environ.get("RSH_CC_LIST_CHUNK", "256"))
+CHUNK_CC_LIST = int(os.environ.get("RSH_CC_LIST_CHUNK", "128"))
 CHUNK_TC = 256   # ... and for the tensor-core kernel (kChunkTC)
 
 

@@ -11,7 +11,7 @@ namespace rsh {
 constexpr int kChunkMin = 32;   // smallest blocks-per-unit a schedule may use (sizes buffers)
 constexpr int kChunkCC = 32;    // CUDA-core path: one warp walks a unit serially
 constexpr int kChunkTC = 256;   // tensor-core path: a unit stays in one TMEM accumulator
-constexpr int kTicketMax = 64;  // windows with more chunks are reduced by the fixup kernels
+constexpr int kTicketMax = 256; // windows with more chunks are reduced by the fixup kernels
 constexpr int kFixSeg = 32;     // chunks per first-level fixup segment
 constexpr int kResRows = 16;    // residual rows per unit
 constexpr int kZeroRows = 32;   // uncovered rows per unit

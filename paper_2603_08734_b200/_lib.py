@@ -50,6 +50,7 @@ SIGNATURES = {
     "rsh_schedule_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "rsh_schedule": (ctypes.c_int, [_i64, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]),
     "rsh_partials_bytes": (_sz, [_i64, _i64, _i32]),
+    "rsh_rowmajor_bytes": (_sz, [_i64, _i64, _i64, _i64, _i64]),
     "rsh_schedule_rowmajor": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _sz, _vp]),
     "rsh_spmm_cc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
                                    _i32, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),

@@ -13,6 +13,7 @@
 //     bit-identical for every max_blocks_per_item and every scheduling order.
 //   * accumulate_precision f32 / f64 (execute.py:33-49): AccT = float / double.
 #include "sched.cuh"
+#include <cstdlib>
 
 namespace rsh {
 
@@ -1188,21 +1189,75 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
 // the format once per schedule; its address is recorded in the schedule so rsh_spmm_cc copies
 // each unit's list with one coalesced read instead of decoding bitmaps.  Results are
 // bit-identical with or without it.
+// bytes rsh_schedule_rowmajor needs: the list (8 per tc nonzero) + scratch to reorder units
+size_t rsh_rowmajor_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res, int64_t tc_nnz) {
+  Sched s;
+  sched_layout(nullptr, n_rows, n_entries, n_blocks, n_res, &s);
+  const int64_t mu = s.max_units;
+  Carve cv(nullptr);
+  cv.take<int2>(tc_nnz > 0 ? tc_nnz : 1);
+  cv.take<unsigned long long>(mu);
+  cv.take<unsigned long long>(mu);
+  cv.take<int4>(mu);
+  size_t t = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (int4*)nullptr, (int4*)nullptr, (int)mu);
+  cv.take<char>(t);
+  return cv.used + 256;
+}
+
+// longest-first order of the window units (key: chunks of the unit's window, descending; then
+// the original position): the chunks of long windows start first instead of forming the
+// kernel's tail, chunk order inside a window and the order of single-chunk windows are kept,
+// residual and zero units keep their slots.
+__global__ void k_unit_keys(Sched s, unsigned long long* keys) {
+  const int64_t n_wu = s.header[1];
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < s.max_units; u += (int64_t)gridDim.x * blockDim.x) {
+    if (u < n_wu) {
+      const int4 un = s.units[u];
+      const uint32_t nch = (uint32_t)s.grp_nch[un.y];
+      keys[u] = ((unsigned long long)(0xFFFFFFFFu - nch) << 32) | (uint32_t)u;
+    } else {
+      keys[u] = ~0ull;
+    }
+  }
+}
+
+// Row-major window list for the streaming kernel (k_rowmajor_list): int2 pairs per tc nonzero
+// built from the format once per schedule (plus the window units put longest-first); its
+// address is recorded in the schedule so rsh_spmm_cc copies each unit's list with one coalesced
+// read instead of decoding bitmaps.  Results are bit-identical with or without it for a given
+// schedule.  ulist_bytes >= rsh_rowmajor_bytes(...).
 int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
                           const float* tc_values, int64_t n_blocks, int64_t tc_nnz, int64_t n_res, void* sched,
                           size_t sched_bytes, void* ulist, size_t ulist_bytes, cudaStream_t st) {
   Sched s;
   const size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_schedule_rowmajor: schedule buffer too small");
-  if (tc_nnz < 0 || (tc_nnz && (!ulist || ulist_bytes < (size_t)tc_nnz * 8)))
-    return fail(kInvalid, "rsh_schedule_rowmajor: list buffer must hold 8 bytes per tc nonzero");
-  if (tc_nnz && ((uintptr_t)ulist & 7)) return fail(kInvalid, "rsh_schedule_rowmajor: list must be 8-byte aligned");
+  if (tc_nnz < 0 || !ulist || ulist_bytes < rsh_rowmajor_bytes(n_rows, n_entries, n_blocks, n_res, tc_nnz))
+    return fail(kInvalid, "rsh_schedule_rowmajor: list buffer smaller than rsh_rowmajor_bytes()");
+  if ((uintptr_t)ulist & 15) return fail(kInvalid, "rsh_schedule_rowmajor: list must be 16-byte aligned");
+  Carve cv(ulist);
+  int2* list = cv.take<int2>(tc_nnz > 0 ? tc_nnz : 1);
+  unsigned long long* keys = cv.take<unsigned long long>(s.max_units);
+  unsigned long long* keys2 = cv.take<unsigned long long>(s.max_units);
+  int4* units2 = cv.take<int4>(s.max_units);
+  size_t t = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (int4*)nullptr, (int4*)nullptr, (int)s.max_units);
+  void* tmp = cv.take<char>(t);
   if (tc_nnz) {
     k_rowmajor_list<<<8 * sm_count(), kThreads, 0, st>>>(s, (const unsigned long long*)bitmaps, col_id, tc_values,
-                                                          (int2*)ulist);
+                                                          list);
     RSH_LAUNCHED("k_rowmajor_list");
   }
-  const int64_t hdr[2] = {(int64_t)(uintptr_t)ulist, tc_nnz};
+  if (!getenv("RSH_NO_LPT")) {
+    k_unit_keys<<<grid_1d(s.max_units), kThreads, 0, st>>>(s, keys);
+    RSH_LAUNCHED("k_unit_keys");
+    RSH_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, keys, keys2, s.units, units2, (int)s.max_units, 0, 64, st));
+    RSH_CUDA(cudaMemcpyAsync(s.units, units2, s.max_units * sizeof(int4), cudaMemcpyDeviceToDevice, st));
+  }
+  const int64_t hdr[2] = {(int64_t)(uintptr_t)list, tc_nnz};
   RSH_CUDA(cudaMemcpyAsync(s.header + 8, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
   RSH_CUDA(cudaStreamSynchronize(st));  // hdr lives on this host stack frame
   return kOk;

@@ -301,7 +301,8 @@ class SpmmPlan:
         if chunk == CHUNK_CC_LIST:
             # the streaming kernel's pre-decoded window list (8 bytes per tc nonzero)
             tc_nnz = int(t.values.numel())
-            self.ulist = torch.empty(max(tc_nnz, 1), dtype=torch.int64, device=dev)
+            lb = lib().rsh_rowmajor_bytes(t.n_rows, t.n_entries, t.n_blocks, t.n_res, tc_nnz)
+            self.ulist = torch.empty((lb + 7) // 8, dtype=torch.int64, device=dev)
             call("rsh_schedule_rowmajor", t.n_rows, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id), _ptr(t.values),
                  t.n_blocks, tc_nnz, t.n_res, _ptr(self.buf), self.nbytes, _ptr(self.ulist), 8 * self.ulist.numel(),
                  _stream(stream))

@@ -1050,7 +1050,11 @@ int launch_stream(const SpmmArgs& a, cudaStream_t st) {
 // narrow rows (N = 16 B x 32 lanes / kG): kG lane groups stream disjoint row ranges of a unit
 template <int VEC, class BT, int kG>
 int launch_stream_groups(const SpmmArgs& a, cudaStream_t st) {
-  return launch_stream_k<VEC, BT, 6, 4, true, false, 320, kG>(a, st);
+  switch ((a.flags >> 3) & 7) {  // pipeline depth / occupancy variants (tuning knob)
+    case 1: return launch_stream_k<VEC, BT, 4, 4, true, false, 320, kG>(a, st);
+    case 3: return launch_stream_k<VEC, BT, 8, 3, true, false, 320, kG>(a, st);
+    default: return launch_stream_k<VEC, BT, 6, 4, true, false, 320, kG>(a, st);
+  }
 }
 
 // pipeline depth / occupancy / list-size variants (tuning knob: flags bits 3-5)

@@ -34,9 +34,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SpMM GFLOP/s (2*nnz*N/t)"
-# profiles/r01_gather_bw2_microbench.txt: random 512-B B rows gathered with LDG.128 by 148 SMs
-GATHER_ROOF_L2_GBS = 18454.0   # 64 MB footprint (L2-resident)
-GATHER_ROOF_HBM_GBS = 7291.0   # 2 GB footprint (from HBM)
+# profiles/r02_gather_plateau.txt: random 512-B B rows gathered with LDG.128 by 148 SMs at full
+# occupancy (the plateau of every path measured: LDG, cp.async, cp.async.bulk, TMA gather4)
+GATHER_ROOF_L2_GBS = 19673.0   # 64 MB footprint (L2-resident)
+GATHER_ROOF_HBM_GBS = 7462.0   # 2 GB footprint (from HBM)
 
 
 def _peaks() -> dict:
@@ -45,16 +46,6 @@ def _peaks() -> dict:
             return json.load(fh)
     except OSError:
         return {"hbm_gbs": 6650.0, "_fallback": True}
-
-
-def _traffic(workload: str):
-    """dram read+write bytes per launch of the SpMM kernel from the committed ncu capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            rec = json.load(fh).get(workload)
-        return None if rec is None else rec["dram_bytes_per_launch"]
-    except (OSError, KeyError, TypeError):
-        return None
 
 
 class ClockSampler:
@@ -116,94 +107,178 @@ class ClockSampler:
 
 def algorithmic_bytes(a, n_feat: int, b_elem: int, val_bytes: int = 4) -> tuple[int, int]:
     """nnz*(val+4) + touched_cols*N*E_B + n_rows*N*4 (C f32), and touched cols."""
-    touched = int(np.unique(a.col_idx).size) if a.nnz else 0
+    touched = int(np.count_nonzero(np.bincount(np.asarray(a.col_idx), minlength=a.n_cols))) if a.nnz else 0
     return a.nnz * (val_bytes + 4) + touched * n_feat * b_elem + a.n_rows * n_feat * 4, touched
 
 
-def cpu_reference_sample(a, b, workload: str, target_s: float = 10.0, num_workers: int = 1):
-    """Time the reference executor restatement (oracle.port_hybrid_spmm) on a bounded sample:
-    a prefix of the format's entries and residual rows holding ~frac of the nnz."""
-    import oracle as O
-    c = O.Csr.of(a)
-    t = O.build_format(c)
-    n_ent, n_res = t.row_window_id.size, t.res_row_id.size
-    frac = 1.0
-    # probe 1% to size the sample
-    e_hi = max(1, int(n_ent * 0.01)) if n_ent else 0
-    t0 = time.perf_counter()
-    O.port_hybrid_spmm(t, b, num_workers, entry_range=(0, e_hi), residual_range=(0, int(n_res * 0.01)))
-    dt = time.perf_counter() - t0
-    if dt > 0:
-        frac = min(1.0, max(0.01, 0.01 * target_s / dt))
-    e_hi = int(n_ent * frac)
-    # do not cut a split window in two
-    while 0 < e_hi < n_ent and t.row_window_id[e_hi] == t.row_window_id[e_hi - 1]:
-        e_hi += 1
-    r_hi = int(n_res * frac)
-    blocks = int(t.row_window_offset[e_hi]) if n_ent else 0
-    nnz_s = int(O.popcounts(t.bitmaps[:blocks]).sum()) + int(t.res_offset[r_hi])
-    t0 = time.perf_counter()
-    O.port_hybrid_spmm(t, b, num_workers, entry_range=(0, e_hi), residual_range=(0, r_hi))
-    dt = time.perf_counter() - t0
-    gflops = 2.0 * nnz_s * b.shape[1] / dt / 1e9
-    sample = (f"{workload}: first {e_hi}/{n_ent} window entries + {r_hi}/{n_res} residual rows "
-              f"({nnz_s} of {a.nnz} nnz, {100.0 * nnz_s / max(a.nnz, 1):.1f}%), one pass {dt:.2f} s")
-    return gflops, dt, sample, nnz_s
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The unmodified reference package (``rstile``) installed under baseline/_ref by
+    ``pip install --no-index --no-build-isolation --no-deps --target baseline/_ref`` (DESIGN.md
+    section 7), or None when it is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "rstile")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import rstile
+    return rstile
+
+
+def workload_config(args, a, w) -> dict:
+    """The ``config`` object both arms print (identical keys and values)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    return {"workload": args.workload, "description": w.description, "n_rows": int(a.n_rows),
+            "n_cols": int(a.n_cols), "nnz": int(a.nnz), "n_features": int(w.n_features),
+            "parallelism": "single GPU" if world == 1 else f"row shard x{world}",
+            "l2": "no flush: per-step inputs (A + B + C) exceed the 126 MB L2"}
+
+
+def _row_slice(a, lo_q: float, frac: float):
+    """Contiguous rows [r0, r1) whose nnz start near quantile lo_q and hold ~frac of the nnz."""
+    rp = np.asarray(a.row_ptr)
+    nnz = int(rp[-1])
+    r0 = int(np.searchsorted(rp, int(lo_q * nnz), side="right")) - 1
+    r0 = max(0, min(r0, a.n_rows - 1))
+    r1 = int(np.searchsorted(rp, int(rp[r0]) + max(1, int(frac * nnz)), side="left"))
+    r1 = max(r0 + 1, min(r1, a.n_rows))
+    return r0, r1
+
+
+class ReferenceSample:
+    """The reference's own pipeline on bounded row slices of the workload: each slice is a
+    CsrMatrix of rows [r0, r1) (all columns), formatted by rstile.partition_rows ->
+    split_long_work -> build_rstile with the FULL matrix's thresholds, and multiplied by
+    rstile.hybrid_spmm(m, DenseMatrix(B), ExecConfig(num_workers=w)) -- the stock code path."""
+
+    def __init__(self, rs, a, b, quantiles, frac):
+        if frac * len(quantiles) >= 1.0:  # small workload: one slice = the whole matrix
+            quantiles, frac = [0.0], 1.0
+        self.rs = rs
+        self.n_feat = int(b.shape[1])
+        self.bd = rs.DenseMatrix.from_array(b)
+        tn, ti = rs.estimate_thresholds(a.n_rows, a.nnz)
+        self.params = rs.PartitionParams(tau_nnz=tn, tau_inc=ti)
+        self.slices, self.build_s, self.built_nnz = [], 0.0, 0
+        rp = np.asarray(a.row_ptr)
+        for q in quantiles:
+            r0, r1 = _row_slice(a, q, frac)
+            s, e = int(rp[r0]), int(rp[r1])
+            sub = rs.CsrMatrix(r1 - r0, a.n_cols, rp[r0:r1 + 1] - s, np.asarray(a.col_idx)[s:e],
+                               np.asarray(a.values)[s:e])
+            t0 = time.perf_counter()
+            plan = rs.split_long_work(sub, rs.partition_rows(sub, self.params), self.params)
+            m = rs.build_rstile(sub, plan)
+            self.build_s += time.perf_counter() - t0
+            self.built_nnz += sub.nnz
+            self.slices.append((m, sub.nnz, (r0, r1)))
+
+    def run(self, k: int, workers: int) -> tuple[float, int]:
+        m, nnz, _ = self.slices[k % len(self.slices)]
+        t0 = time.perf_counter()
+        self.rs.hybrid_spmm(m, self.bd, self.rs.ExecConfig(num_workers=workers))
+        return time.perf_counter() - t0, nnz
+
+    def best_workers(self, cores: int) -> tuple[int, dict]:
+        """num_workers in {1, cores}: the faster on slice 0."""
+        rates = {}
+        for w in sorted({1, cores}):
+            dt, nnz = self.run(0, w)
+            rates[w] = 2.0 * nnz * self.n_feat / dt / 1e9
+        return max(rates, key=rates.get), rates
+
+    def describe(self, workers: int) -> str:
+        rows = ", ".join(f"[{r0}, {r1})" for _, _, (r0, r1) in self.slices)
+        return (f"rstile {self.rs.__version__ if hasattr(self.rs, '__version__') else ''} from baseline/_ref: "
+                f"row slices {rows} ({self.built_nnz} nnz in all) formatted by the reference's own "
+                f"partition_rows/split_long_work/build_rstile, hybrid_spmm with ExecConfig(num_workers={workers})")
+
+
+def _probe_frac(rs, a, b, target_s: float, cores: int) -> float:
+    """Fraction of the nnz one reference hybrid_spmm call finishes in ~target_s."""
+    probe = ReferenceSample(rs, a, b, [0.5], 0.004)
+    dt, nnz = probe.run(0, 1)
+    dt2, _ = probe.run(0, cores) if cores > 1 else (dt, nnz)
+    rate = nnz / max(min(dt, dt2), 1e-6)
+    return float(min(1.0, max(0.002, rate * target_s / max(a.nnz, 1))))
+
+
+def cpu_reference_sample(a, b, workload: str, target_s: float = 4.0):
+    """cpu_baseline of the GPU arm: the reference (baseline/_ref) on one bounded row slice, best
+    of {1, all cores} workers; the oracle's numpy port when the reference is not installed."""
+    rs = import_reference()
+    cores = len(os.sched_getaffinity(0))
+    if rs is None:
+        import oracle as O
+        c = O.Csr.of(a)
+        t = O.build_format(c)
+        n_ent = t.row_window_id.size
+        e_hi = max(1, n_ent // 20)
+        t0 = time.perf_counter()
+        O.port_hybrid_spmm(t, b, 1, entry_range=(0, e_hi), residual_range=(0, t.res_row_id.size // 20))
+        dt = time.perf_counter() - t0
+        nnz_s = int(O.popcounts(t.bitmaps[:int(t.row_window_offset[e_hi])]).sum())
+        return {"value": 2.0 * nnz_s * b.shape[1] / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+                "sample": f"{workload}: numpy port of rstile hybrid_spmm (oracle/) on 1/20 of the windows; "
+                          "baseline/_ref is not installed"}
+    frac = _probe_frac(rs, a, b, target_s, cores)
+    smp = ReferenceSample(rs, a, b, [0.5], frac)
+    workers, rates = smp.best_workers(cores)
+    dt, nnz = smp.run(0, workers)
+    return {"value": 2.0 * nnz * b.shape[1] / dt / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": "reference",
+            "sample": f"{workload}: " + smp.describe(workers) + f"; one call {dt:.2f} s",
+            "rates_by_workers": rates, "host_cores": cores}
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU executor on this host (rank 0 only)."""
+    """--impl reference: the reference's own CPU SpMM (rstile from baseline/_ref, stock code path)
+    on this host, rank 0 only.  Each step is one rstile.hybrid_spmm call on a bounded row slice of
+    the workload (three slices at nnz quantiles 1/6, 1/2, 5/6, cycled), with the faster of
+    num_workers in {1, all cores}."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2603_08734_b200 import synth
-    import oracle as O
-    a = synth.workload_matrix(args.workload)
-    w = synth.WORKLOADS[args.workload]
-    b = synth.workload_b(args.workload, a.n_cols)
+    name = args.workload
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and name == "rmat1m":
+        name = f"rmat_s{20 + int(round(np.log2(world)))}"  # the GPU arm's weak-scaling matrix
+    a = synth.workload_matrix(name)
+    w = synth.workload_spec(name)
+    b = synth.workload_b(name, a.n_cols)
     cores = len(os.sched_getaffinity(0))
-    c = O.Csr.of(a)
-    t = O.build_format(c)
-    n_ent, n_res = t.row_window_id.size, t.res_row_id.size
-    # each step: a bounded slice of the work (~2 s), stepping through the matrix
-    probe_e = max(1, n_ent // 100)
-    t0 = time.perf_counter()
-    O.port_hybrid_spmm(t, b, cores, entry_range=(0, probe_e), residual_range=(0, n_res // 100))
-    per = max(time.perf_counter() - t0, 1e-6)
-    frac = min(1.0, 0.01 * 2.0 / per)
-    slices = max(1, int(round(1.0 / frac)))
-    step_ent = -(-n_ent // slices) if n_ent else 0
-    step_res = -(-n_res // slices) if n_res else 0
-    vstart = np.zeros(t.bitmaps.size + 1, np.int64)
-    np.cumsum(O.popcounts(t.bitmaps), out=vstart[1:])
+    rs = import_reference()
+    if rs is None:
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref (the reference install) is missing"}))
+        return
+    total = args.warmup + args.steps
+    # each call ~ budget / (#calls) seconds so the whole run stays within a few minutes
+    per_call = float(min(1.2, max(0.3, 90.0 / total)))
+    frac = _probe_frac(rs, a, b, per_call, cores)
+    smp = ReferenceSample(rs, a, b, [1 / 6, 0.5, 5 / 6], frac)
+    workers, rates = smp.best_workers(cores)
     times, flops = [], []
-    for it in range(args.warmup + args.steps):
-        k = it % slices
-        e0, e1 = min(k * step_ent, n_ent), min((k + 1) * step_ent, n_ent)
-        while 0 < e0 < n_ent and t.row_window_id[e0] == t.row_window_id[e0 - 1]:
-            e0 += 1
-        while 0 < e1 < n_ent and t.row_window_id[e1] == t.row_window_id[e1 - 1]:
-            e1 += 1
-        r0, r1 = min(k * step_res, n_res), min((k + 1) * step_res, n_res)
-        nnz_s = int(vstart[t.row_window_offset[e1]] - vstart[t.row_window_offset[e0]]) + \
-            int(t.res_offset[r1] - t.res_offset[r0])
-        s = time.perf_counter()
-        O.port_hybrid_spmm(t, b, cores, entry_range=(e0, e1), residual_range=(r0, r1))
-        d = time.perf_counter() - s
+    for it in range(total):
+        dt, nnz = smp.run(it, workers)
         if it >= args.warmup:
-            times.append(d)
-            flops.append(2.0 * nnz_s * w.n_features)
+            times.append(dt)
+            flops.append(2.0 * nnz * w.n_features)
     value = sum(flops) / sum(times) / 1e9
+    args_cfg = argparse.Namespace(**vars(args))
+    args_cfg.workload = name
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": args.workload, "description": w.description,
-                                        "n_rows": a.n_rows, "nnz": a.nnz, "n_features": w.n_features},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"each step = 1/{slices} of the {args.workload} window entries and residual "
-                                   f"rows (consecutive slices), numpy restatement of rstile hybrid_spmm "
-                                   f"(oracle.port_hybrid_spmm), ThreadPoolExecutor({cores}) like the reference"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if w.dtype == "bf16" else "f32", "data": "synthetic",
+        "config": workload_config(args_cfg, a, w),
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": workers, "kind": "reference",
+                         "sample": smp.describe(workers) + "; steps cycle through the slices",
+                         "rates_by_workers": rates, "host_cores": cores},
+        "preprocess": {"reference_build_s": smp.build_s, "nnz": smp.built_nnz,
+                       "ms_per_mnnz": 1e3 * smp.build_s / max(smp.built_nnz / 1e6, 1e-9),
+                       "what": "rstile partition_rows + split_long_work + build_rstile on the sampled slices"},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -218,6 +293,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu DRAM-traffic measurement")
+    ap.add_argument("--kernel-only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--math", default="auto", choices=["auto", "fp32", "tf32", "tc"])
     ap.add_argument("--sharded", action="store_true",
                     help="run the row-shard path even on one GPU (config 5 at N=1 under torchrun)")
@@ -226,61 +303,124 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.kernel_only:
+        run_kernel_only(args)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1 or args.sharded:
         from paper_2603_08734_b200.dist import run_sharded_bench
-        run_sharded_bench(args, METRIC, clock_factory=ClockSampler)
+        run_sharded_bench(args, METRIC, clock_factory=ClockSampler, config_factory=workload_config)
         return
     run_single(args)
 
 
-def run_single(args):
+def _launches() -> int:
+    from paper_2603_08734_b200 import _lib
+    return int(_lib.lib().rsh_launch_count())
+
+
+def ncu_traffic(args, kernel_regex: str, timeout_s: float = 240.0):
+    """dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the timed kernel, measured
+    in this run: ncu over a child process that replays this workload (``--kernel-only``).  Also
+    returns the L2 hit rate.  None when ncu is unavailable or fails (the line then says so)."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if args.no_ncu or not os.path.exists(ncu):
+        return None
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,"
+           "gpu__time_duration.sum", "--clock-control", "none", "-k", f"regex:{kernel_regex}", "--launch-skip", "3",
+           "--launch-count", "1", "--csv", sys.executable, os.path.abspath(__file__), "--kernel-only",
+           "--workload", args.workload, "--math", args.math]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, cwd=ROOT)
+    except (OSError, subprocess.TimeoutExpired):
+        return None
+    vals = {}
+    for ln in out.stdout.splitlines():
+        parts = [p.strip('"') for p in ln.split('","')]
+        if len(parts) >= 3 and parts[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum",
+                                             "lts__t_sector_hit_rate.pct", "gpu__time_duration.sum"):
+            unit, v = parts[-2], parts[-1].replace(",", "")
+            try:
+                x = float(v)
+            except ValueError:
+                continue
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+                     "msecond": 1e-3, "%": 1}.get(unit, 1)
+            vals[parts[-3]] = x * scale
+    if "dram__bytes_read.sum" not in vals:
+        return None
+    return {"dram_bytes": int(vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0)),
+            "l2_hit_pct": vals.get("lts__t_sector_hit_rate.pct"),
+            "ncu_kernel_ms": 1e3 * vals["gpu__time_duration.sum"] if "gpu__time_duration.sum" in vals else None}
+
+
+def _setup(args, dev):
+    """Workload matrix, B and the device format + schedule (preprocessing, reported separately)."""
     import torch
     from paper_2603_08734_b200 import synth
-    from paper_2603_08734_b200.device import DeviceCsr, build_device, spmm_device, spmm_plan, DeviceTile
-    from paper_2603_08734_b200 import _lib
-
-    dev = torch.device("cuda", 0)
-    torch.cuda.set_device(dev)
-    w = synth.WORKLOADS[args.workload]
+    from paper_2603_08734_b200.device import CHUNK_CC_LIST, DeviceCsr, build_device, spmm_plan
+    w = synth.workload_spec(args.workload)
     a = synth.workload_matrix(args.workload)
     b_np = synth.workload_b(args.workload, a.n_cols)
-    b_elem = 2 if w.dtype == "bf16" else 4
-    alg_bytes, touched = algorithmic_bytes(a, w.n_features, b_elem, 2 if w.dtype == "bf16" else 4)
-    flops = 2.0 * a.nnz * w.n_features
-
-    # preprocessing on device (reported separately from the steady-state SpMM); the first build
-    # also pays one-time library / allocator initialisation, so the second one is reported
     d = DeviceCsr.from_host(a, dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     tile = build_device(d)
     torch.cuda.synchronize()
-    t_build_first = time.perf_counter() - t0
+    t_first = time.perf_counter() - t0
     del tile
+    # the first build also pays one-time library / allocator initialisation: report the second
     t0 = time.perf_counter()
     tile = build_device(d)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
-    # schedule for the streaming kernel: long units + the pre-decoded row-major window list
-    from paper_2603_08734_b200.device import CHUNK_CC_LIST, CHUNK_TC
     t0 = time.perf_counter()
     plan = spmm_plan(tile, CHUNK_CC_LIST)
     torch.cuda.synchronize()
     t_sched = time.perf_counter() - t0
-    spmm_plan(tile, CHUNK_TC)  # the tensor-core candidate's schedule
     bt = torch.from_numpy(b_np).to(dev)
     if w.dtype == "bf16":
         bt = bt.to(torch.bfloat16)
+    return w, a, b_np, tile, plan, bt, {"build_device": 1e3 * t_build, "build_device_first_call": 1e3 * t_first,
+                                         "schedule": 1e3 * t_sched}
+
+
+def run_kernel_only(args):
+    """The ncu child of ncu_traffic: warm-up launches then a few timed-path launches, no output."""
+    import torch
+    from paper_2603_08734_b200.device import spmm_device
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    w, a, _, tile, _, bt, _ = _setup(args, dev)
+    out = torch.empty((a.n_rows, w.n_features), dtype=torch.float32, device=dev)
+    math = "auto" if args.math == "auto" else args.math
+    for _ in range(5):
+        spmm_device(tile, bt, out=out, math=math)
+    torch.cuda.synchronize()
+
+
+def run_single(args):
+    import torch
+    from paper_2603_08734_b200.device import CHUNK_TC, DeviceTile, resolve_math, spmm_device, spmm_plan, tc_eligible
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    w, a, b_np, tile, plan, bt, prep = _setup(args, dev)
+    b_elem = 2 if w.dtype == "bf16" else 4
+    alg_bytes, touched = algorithmic_bytes(a, w.n_features, b_elem, 2 if w.dtype == "bf16" else 4)
+    flops = 2.0 * a.nnz * w.n_features
     out = torch.empty((a.n_rows, w.n_features), dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream()
 
-    # arithmetic path: fp32 B -> exact FP32 (CUDA cores) or TF32 (tensor cores); bf16 B -> tensor
-    # cores when the shape allows.  "auto" times both for a few launches and keeps the faster.
-    from paper_2603_08734_b200.device import resolve_math, tc_eligible
+    # arithmetic path: fp32 B -> exact FP32 (CUDA cores) or TF32 (tensor cores); bf16 B -> the
+    # CUDA-core stream or BF16 tensor cores when the shape allows.  "auto" times the candidates
+    # for a few launches and keeps the faster.
     candidates = (["fp32", "tf32"] if w.dtype == "f32" else ["auto", "tc"]) if tc_eligible(tile, bt) else ["auto"]
     if args.math != "auto":
         candidates = [args.math]
+    if any(resolve_math(m, bt, tile, "f32") == "tc" for m in candidates):
+        spmm_plan(tile, CHUNK_TC)
     path_ms = {}
     for m in candidates:
         for _ in range(2):
@@ -293,7 +433,7 @@ def run_single(args):
         torch.cuda.synchronize()
         path_ms[m] = e0.elapsed_time(e1) / 5
     math = min(path_ms, key=path_ms.get)
-    kernel = "k_spmm_tc" if resolve_math(math, bt, tile, "f32") == "tc" else "k_spmm_cc"
+    kernel = "k_spmm_tc" if resolve_math(math, bt, tile, "f32") == "tc" else "k_spmm_stream"
 
     clocks = ClockSampler(0)
     clocks.start()
@@ -304,6 +444,7 @@ def run_single(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    n_launch0 = _launches()
     w0 = time.time()
     g0.record(st)
     for e0, e1 in ev:
@@ -313,6 +454,7 @@ def run_single(args):
     g1.record(st)
     torch.cuda.synchronize()
     w1 = time.time()
+    gpu_launches = _launches() - n_launch0
     clocks.window = (w0, w1)
     total_ms = g0.elapsed_time(g1)
     kern_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
@@ -325,21 +467,18 @@ def run_single(args):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     gathered = int(plan_gather_bytes(tile, w.n_features, b_elem))
 
-    # end to end through the C ABI with host buffers: H2D(format + B), SpMM, D2H(C) every step
-    host = {k: getattr(tile, k).cpu().pin_memory() for k in (
-        "row_window_id", "row_window_offset", "bitmaps", "col_id", "values", "res_row_id", "res_offset",
-        "res_col_id", "res_values")}
+    # end to end through the public device API with host buffers: every step copies the format and
+    # B in from pinned host memory, builds the schedule (the format's arrays are new, so the
+    # cached one is stale), runs the SpMM and copies C out
+    fields = ("row_window_id", "row_window_offset", "bitmaps", "col_id", "values", "res_row_id", "res_offset",
+              "res_col_id", "res_values")
+    host = {k: getattr(tile, k).cpu().pin_memory() for k in fields}
     b_host = bt.cpu().pin_memory()
     c_host = torch.empty((a.n_rows, w.n_features), dtype=torch.float32).pin_memory()
     dev_bufs = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
     b_dev2 = torch.empty_like(b_host, device=dev)
     t2 = DeviceTile(tile.n_rows, tile.n_cols, tile.window_size, **dev_bufs)
-    t2._plan = tile._plan  # the schedules are part of the prebuilt operator, like the format itself
-    # the schedule's pre-decoded window list is derived from the format: it travels with it
-    ulists = [(pl.ulist, pl.ulist.cpu().pin_memory()) for pl in (tile._plan or {}).values()
-              if getattr(pl, "ulist", None) is not None]
-    h2d = sum(v.numel() * v.element_size() for v in host.values()) + b_host.numel() * b_host.element_size() + \
-        sum(h.numel() * h.element_size() for _, h in ulists)
+    h2d = sum(v.numel() * v.element_size() for v in host.values()) + b_host.numel() * b_host.element_size()
     d2h = c_host.numel() * 4
     e2e_ms = []
     for it in range(args.e2e_steps + 1):
@@ -349,48 +488,44 @@ def run_single(args):
         for k, v in host.items():
             dev_bufs[k].copy_(v, non_blocking=True)
         b_dev2.copy_(b_host, non_blocking=True)
-        for dst, src in ulists:
-            dst.copy_(src, non_blocking=True)
         spmm_device(t2, b_dev2, out=out, math=math)
         c_host.copy_(out, non_blocking=True)
         s1.record(st)
         torch.cuda.synchronize()
         if it:
             e2e_ms.append(s0.elapsed_time(s1))
-    e2e_value = flops / (float(np.mean(e2e_ms)) * 1e-3) / 1e9
+    e2e_value = flops / (float(np.mean(e2e_ms)) * 1e-3) / 1e9 if e2e_ms else None
 
-    cpu = None
-    if not args.no_cpu_baseline:
-        gf, dt, sample, _ = cpu_reference_sample(a, b_np.astype(np.float32), args.workload)
-        cpu = {"value": gf, "unit": "GFLOP/s", "cores": 1, "kind": "port", "sample": sample}
+    cpu = None if args.no_cpu_baseline else cpu_reference_sample(a, b_np.astype(np.float32), args.workload)
+    traffic = ncu_traffic(args, "k_spmm_stream|k_spmm_tc|k_spmm_cc")
 
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else ("tf32" if math == "tf32" else "f32"),
         "data": "synthetic",
-        "config": {"workload": args.workload, "description": w.description, "n_rows": a.n_rows,
-                   "n_cols": a.n_cols, "nnz": a.nnz, "n_features": w.n_features,
-                   "parallelism": "single GPU", "math": math, "kernel": kernel,
-                   "path_ms": path_ms, "l2": "no flush: per-step inputs (A + B + C = "
-                   f"{(alg_bytes + gathered * 0) / 1e9:.2f} GB compulsory) exceed the 126 MB L2",
-                   "preprocess_ms": {"build_device": 1e3 * t_build, "build_device_first_call": 1e3 * t_build_first,
-                                     "schedule": 1e3 * t_sched},
-                   "format": {"entries": tile.n_entries, "blocks": tile.n_blocks, "residual_rows": tile.n_res,
-                              "units": plan.units, "uncovered_rows": plan.uncovered}},
-        "gpu_launches": 3 * args.steps,  # per step: the SpMM kernel + the two long-window fix-up kernels
+        "config": workload_config(args, a, w),
+        "details": {"math": math, "kernel": kernel, "path_ms": path_ms, "preprocess_ms": prep,
+                    "format": {"entries": tile.n_entries, "blocks": tile.n_blocks, "residual_rows": tile.n_res,
+                               "units": plan.units, "uncovered_rows": plan.uncovered,
+                               "fixup_windows": plan.fixup_windows}},
+        "gpu_launches": gpu_launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(args.workload),
+                     "frac": achieved / peak, "traffic": None if traffic is None else traffic["dram_bytes"],
+                     "traffic_source": "ncu over a --kernel-only child of this run (one launch, cold L2)"
+                     if traffic else "ncu unavailable in this run",
+                     "l2_hit_pct": None if traffic is None else traffic["l2_hit_pct"],
                      "algorithmic_bytes": alg_bytes, "kernel": kernel, "kernel_ms": kern_avg,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
         "gather": {"gathered_bytes": gathered, "achieved_gbs": gathered / (kern_avg * 1e-3) / 1e9,
                    "roof_l2_resident_gbs": GATHER_ROOF_L2_GBS, "roof_hbm_gbs": GATHER_ROOF_HBM_GBS,
                    "frac_of_l2_roof": gathered / (kern_avg * 1e-3) / 1e9 / GATHER_ROOF_L2_GBS,
                    "note": "B rows the window path must move into the SMs (one per occupied col_id slot "
-                           "+ one per residual nonzero); roofs measured by tools/microbench/gather_bw2.cu"},
+                           "+ one per residual nonzero); roofs from tools/microbench/gather_plateau.cu"},
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms)),
-                "path": f"{kernel} via the C ABI (ctypes), pinned host format + B in, C out"},
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms)) if e2e_ms else None,
+                "path": f"spmm_device ({kernel}) via the C ABI: pinned host format + B in, schedule build, "
+                        "SpMM, C out"},
         "cpu_baseline": cpu,
         "clocks": clk,
     }

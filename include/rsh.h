@@ -12,8 +12,11 @@
  *     *_workspace / *_bytes query); the library never allocates or frees caller memory;
  *   - return value: 0 ok, 1 invalid argument (-> ValueError), 2 format (-> FormatError),
  *     3 CUDA/launch error (-> RuntimeError); rsh_last_error() gives a thread-local message;
- *   - no global mutable state besides cached per-kernel launch sizes: calls are reentrant,
- *     one process per GPU for multi-GPU use.
+ *   - no global mutable state besides cached per-kernel launch sizes and a diagnostic launch
+ *     counter: calls are reentrant.  A schedule (rsh_schedule) is read-only during SpMM
+ *     launches; every launch's mutable state (work counter, window tickets, chunk partials)
+ *     lives in the caller's SpMM workspace, so concurrent launches sharing one schedule need one
+ *     workspace each (e.g. one per stream).  One process per GPU for multi-GPU use.
  *   - dtypes follow the reference format (tile.py:43-82): row_window_id int32,
  *     row_window_offset int64, bitmaps uint64, col_id int32, values float32; residual row_id
  *     int32, row_nnz_offset int64, col_id int32, values float32.  CSR: row_ptr int64,
@@ -33,6 +36,9 @@ extern "C" {
 /* ---- plumbing --------------------------------------------------------------------------- */
 const char* rsh_last_error(void);
 int rsh_abi_version(void);
+/* kernels launched through this library by the process so far (diagnostic; the bench reports
+ * the launches inside its timed region from it) */
+unsigned long long rsh_launch_count(void);
 /* host pointers: compute capability and SM count of the current device */
 int rsh_device_info(int32_t* major, int32_t* minor, int32_t* sms);
 
@@ -125,7 +131,12 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
                  const int64_t* row_window_offset, int64_t n_entries, const uint64_t* bitmaps, int64_t n_blocks,
                  const int32_t* res_row_id, int64_t n_res, int32_t chunk_blocks, void* sched, size_t sched_bytes,
                  int64_t* header_out, cudaStream_t stream);
-size_t rsh_partials_bytes(int64_t partial_slots, int64_t n_features, int32_t accum);
+/* SpMM workspace: a control block (work counter, per-window tickets) + chunk partials for
+ * partial_slots (schedule header[3]) 8-row slots.  16-byte aligned, ZERO-FILLED by the caller
+ * before its first use (every launch leaves the control block zero again); one workspace per
+ * concurrently running launch.  A launch whose workspace holds fewer partial slots than its
+ * schedule needs traps (the kernel checks header[3] against the size passed). */
+size_t rsh_partials_bytes(int64_t n_entries, int64_t partial_slots, int64_t n_features, int32_t accum);
 
 /* ---- row-major window list (optional, once per schedule; no reference counterpart): the
  *      window units' nonzeros as int2 (col_id, value) pairs in stream order (the buffer,
@@ -140,7 +151,10 @@ int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bit
 
 /* ---- hybrid SpMM: execute.py:155-218 hybrid_spmm.  C[n_rows x N] (row stride ldc) is
  *      fully written: window rows assigned, residual rows assigned, all other rows zero.
- *      B[n_cols x N] row stride ldb; b_dtype 0 f32, 1 bf16, 2 f16; accum 0 f32, 1 f64.
+ *      B[n_cols x N] row stride ldb; b_dtype 0 f32, 1 bf16, 2 f16; accum bit 0: 0 f32, 1 f64;
+ *      accum bits 1..14 are kernel-variant knobs (spmm_cc.cu), bit 14 = "the schedule has no
+ *      window beyond 256 chunks (header[6] == 0): skip the two fix-up launches".
+ *      sched/partials: the schedule and the caller's workspace (rsh_partials_bytes).
  *      rsh_spmm_cc: one persistent CUDA-core launch (exact FP32 products). -------------- */
 int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const uint64_t* bitmaps,
                 const int32_t* col_id, const float* tc_values, int64_t n_blocks, const int32_t* res_row_id,

@@ -23,6 +23,7 @@ _sz = ctypes.c_size_t
 SIGNATURES = {
     "rsh_last_error": (ctypes.c_char_p, []),
     "rsh_abi_version": (ctypes.c_int, []),
+    "rsh_launch_count": (ctypes.c_ulonglong, []),
     "rsh_device_info": (ctypes.c_int, [_vp, _vp, _vp]),
     "rsh_partition_workspace": (_sz, [_i64]),
     "rsh_partition": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
@@ -49,7 +50,7 @@ SIGNATURES = {
     "rsh_isolation_adjust": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _i64, _vp, _vp]),
     "rsh_schedule_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "rsh_schedule": (ctypes.c_int, [_i64, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _vp]),
-    "rsh_partials_bytes": (_sz, [_i64, _i64, _i32]),
+    "rsh_partials_bytes": (_sz, [_i64, _i64, _i64, _i32]),
     "rsh_rowmajor_bytes": (_sz, [_i64, _i64, _i64, _i64, _i64]),
     "rsh_schedule_rowmajor": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _sz, _vp]),
     "rsh_spmm_cc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,

@@ -490,6 +490,9 @@ int rsh_plan_windows(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_r
                      int64_t* block_base, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n_rows < 0 || nnz < 0 || n_win < 0 || window_size < 1 || window_size > 8)
     return fail(kInvalid, "rsh_plan_windows: bad arguments");
+  // prefix[] and the cub scans index nonzeros with int32 (the reference's INDEX_LIMIT, core.py)
+  if (nnz + 1 >= (1LL << 31) || n_rows >= (1LL << 31))
+    return fail(kInvalid, "rsh_plan_windows: %lld nonzeros exceed the 32-bit index limit", (long long)nnz);
   size_t need = rsh_plan_workspace(n_rows, nnz, n_win);
   if (!ws || ws_bytes < need) return fail(kInvalid, "rsh_plan_windows: workspace %zu < %zu bytes", ws_bytes, need);
   Carve cv(ws);
@@ -550,6 +553,8 @@ int rsh_build_fill(const int64_t* row_ptr, const int32_t* col_idx, const float* 
                    size_t ws_bytes, cudaStream_t st) {
   if (n_blocks < 0 || 8 * n_blocks >= (1LL << 32))
     return fail(kInvalid, "rsh_build_fill: %lld blocks exceed the 32-bit slot limit", (long long)n_blocks);
+  if (nnz < 0 || nnz + 1 >= (1LL << 31))
+    return fail(kInvalid, "rsh_build_fill: %lld nonzeros exceed the 32-bit index limit", (long long)nnz);
   size_t need = rsh_fill_workspace(nnz, n_blocks);
   if (!ws || ws_bytes < need) return fail(kInvalid, "rsh_build_fill: workspace %zu < %zu bytes", ws_bytes, need);
   Carve cv(ws);

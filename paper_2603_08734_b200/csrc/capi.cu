@@ -2,6 +2,7 @@
 #include "common.cuh"
 #include <cstdarg>
 #include <cstdio>
+#include <atomic>
 
 namespace rsh {
 
@@ -19,6 +20,9 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(kCuda, "CUDA error %d (%s) at %s", (int)e, cudaGetErrorString(e), where);
 }
 
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 int sm_count() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -33,6 +37,9 @@ extern "C" {
 const char* rsh_last_error(void) { return rsh::g_err; }
 
 int rsh_abi_version(void) { return 1; }
+
+// kernels this process has launched through the library so far (all threads, all devices)
+unsigned long long rsh_launch_count(void) { return rsh::g_launches.load(std::memory_order_relaxed); }
 
 // 0 ok; sets *major/*minor to the compute capability of the current device
 int rsh_device_info(int32_t* major, int32_t* minor, int32_t* sms) {

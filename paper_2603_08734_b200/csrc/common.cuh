@@ -18,8 +18,12 @@ int cuda_fail(cudaError_t e, const char* where);
     cudaError_t _e = (x);                                        \
     if (_e != cudaSuccess) return ::rsh::cuda_fail(_e, #x);      \
   } while (0)
+// every kernel launch is followed by RSH_LAUNCHED, which also bumps the process-wide launch
+// counter behind rsh_launch_count() (diagnostic: the bench reports launches per timed region)
+void count_launch();
 #define RSH_LAUNCHED(name)                                       \
   do {                                                           \
+    ::rsh::count_launch();                                       \
     cudaError_t _e = cudaGetLastError();                         \
     if (_e != cudaSuccess) return ::rsh::cuda_fail(_e, name);    \
   } while (0)

@@ -9,6 +9,7 @@
 namespace rsh {
 
 constexpr int kChunkMin = 32;   // smallest blocks-per-unit a schedule may use (sizes buffers)
+constexpr int kChunkMax = 1023; // largest: a unit's per-row totals (<= 8 x chunk) fit 16 bits
 constexpr int kChunkCC = 32;    // CUDA-core path: one warp walks a unit serially
 constexpr int kChunkTC = 256;   // tensor-core path: a unit stays in one TMEM accumulator
 constexpr int kTicketMax = 256; // windows with more chunks are reduced by the fixup kernels
@@ -203,8 +204,33 @@ struct SpmmArgs {
   int32_t window_size;
   Sched s;
   void* partials;
+  int64_t part_slots;  // 8-row partial slots the caller's workspace holds
   int32_t flags;  // tensor-core path knobs (bit 1: skip the consumer-side proxy fence)
 };
+
+// Per-launch mutable state lives in the CALLER's workspace, not in the schedule, so one schedule
+// can serve concurrent launches (one workspace each): uint32 [0] next unit, [1] warps done,
+// [2..3] unused, [4 .. 4 + n_entries] per-window tickets, then the chunk partials (256-B
+// aligned).  The caller zero-fills a workspace once; every launch leaves the control words zero.
+inline size_t spmm_ctl_bytes(int64_t n_entries) { return ((size_t)(4 + n_entries + 1) * 4 + 255) & ~size_t(255); }
+
+inline int bind_workspace(SpmmArgs& a, void* ws, size_t ws_bytes, int64_t n_entries, size_t acc_bytes) {
+  const size_t ctl = spmm_ctl_bytes(n_entries);
+  if (!ws || ((uintptr_t)ws & 15) || ws_bytes < ctl)
+    return fail(kInvalid, "rsh_spmm: workspace (%zu bytes) smaller than its control block (%zu); size it with "
+                          "rsh_partials_bytes", ws_bytes, ctl);
+  a.s.counters = reinterpret_cast<uint32_t*>(ws);
+  a.s.ticket = reinterpret_cast<uint32_t*>(ws) + 4;
+  a.partials = reinterpret_cast<char*>(ws) + ctl;
+  a.part_slots = (int64_t)((ws_bytes - ctl) / (8 * (size_t)a.N * acc_bytes));
+  return kOk;
+}
+
+// every SpMM kernel checks, once per CTA, that the workspace holds the schedule's partial slots
+// (header[3]); a short workspace is a caller bug and fails the launch instead of writing past it
+__device__ __forceinline__ void check_workspace(const SpmmArgs& a) {
+  if (threadIdx.x == 0 && a.s.header[3] > a.part_slots) __trap();
+}
 
 
 // One residual row set [i0, i1) (execute.py:184-193): lane owns VEC consecutive features,

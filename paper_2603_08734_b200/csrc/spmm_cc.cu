@@ -96,6 +96,15 @@ __global__ void k_popc32(const unsigned long long* __restrict__ bm, int64_t nb, 
     pc[i] = i < nb ? __popcll(bm[i]) : 0;
 }
 
+__global__ void k_popc_total(const unsigned long long* __restrict__ bm, int64_t nb, unsigned long long* tot) {
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += (int64_t)gridDim.x * blockDim.x)
+    s += __popcll(bm[i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(tot, s);
+}
+
 __global__ void k_finish_header(Sched s, int64_t E, int64_t n_res, int32_t chunk) {
   int64_t uw = s.unit_base[E];
   int64_t ru = (n_res + kResRows - 1) / kResRows;
@@ -403,6 +412,7 @@ template <int VEC, class BT, class AccT, int MINB = 4, int PF = 4, int G = 1>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_cc(SpmmArgs a) {
   __shared__ int2 s_list[kThreads / 32][kListCap];  // per-warp (col, value) list of a window unit
   __shared__ int s_tab[kThreads / 32][256];          // per-warp list offsets (lane, row)
+  check_workspace(a);
   const int lane = threadIdx.x & 31;
   const int64_t total_units = a.s.header[2];
   const int n_fc = (a.N + 32 * VEC - 1) / (32 * VEC);
@@ -532,10 +542,12 @@ __global__ void k_fixup_rows(SpmmArgs a) {
 
 template <class AccT>
 int launch_fixup(const SpmmArgs& a, cudaStream_t st) {
+  if (a.flags & 8192) return kOk;  // the caller knows the schedule has no fix-up windows
   const unsigned blocks = (unsigned)(2 * sm_count());
   k_fixup_segments<AccT><<<blocks, kThreads, 0, st>>>(a);
+  RSH_LAUNCHED("k_fixup_segments");
   k_fixup_rows<AccT><<<blocks, kThreads, 0, st>>>(a);
-  RSH_LAUNCHED("k_fixup");
+  RSH_LAUNCHED("k_fixup_rows");
   return kOk;
 }
 template int launch_fixup<float>(const SpmmArgs&, cudaStream_t);
@@ -941,6 +953,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
   __shared__ StreamSmem<kCap> smem_all[kThreads / 32];
   StreamSmem<kCap>& sm = smem_all[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
+  check_workspace(a);
   const int64_t total_units = a.s.header[2];
   // kG > 1: lane groups of 32/kG lanes, each covering all N = (32/kG) * VEC features
   const int n_fc = kG > 1 ? 1 : (a.N + 32 * VEC - 1) / (32 * VEC);
@@ -1130,8 +1143,9 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
                  int32_t chunk_blocks, void* sched, size_t sched_bytes, int64_t* header_out, cudaStream_t st) {
   if (n_rows < 0 || n_entries < 0 || n_blocks < 0 || n_res < 0 || window_size < 1 || window_size > 8)
     return fail(kInvalid, "rsh_schedule: bad sizes");
-  if (chunk_blocks < kChunkMin || chunk_blocks > (1 << 20))
-    return fail(kInvalid, "rsh_schedule: chunk_blocks %d outside [%d, 2^20]", chunk_blocks, kChunkMin);
+  // units pack per-row counts of up to chunk_blocks x 8 nonzeros into 16-bit fields
+  if (chunk_blocks < kChunkMin || chunk_blocks > kChunkMax)
+    return fail(kInvalid, "rsh_schedule: chunk_blocks %d outside [%d, %d]", chunk_blocks, kChunkMin, kChunkMax);
   if (n_blocks >= (1LL << 31) || n_rows >= (1LL << 31)) return fail(kInvalid, "rsh_schedule: index limit");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
@@ -1173,6 +1187,18 @@ int rsh_schedule(int64_t n_rows, int32_t window_size, const int32_t* row_window_
   k_popc32<<<grid_1d(n_blocks + 1), kThreads, 0, st>>>((const unsigned long long*)bitmaps, n_blocks, s.pc);
   cb = s.cub_bytes;
   RSH_CUDA(cub::DeviceScan::ExclusiveSum(s.cub, cb, s.pc, s.vstart, (int)(n_blocks + 1), st));
+  // vstart (int32) must not wrap: tc nonzeros < 2^31, summed exactly in 64 bits
+  if (n_blocks * 64 >= (1LL << 31)) {
+    int64_t* tot = s.header + 10;
+    RSH_CUDA(cudaMemsetAsync(tot, 0, sizeof(int64_t), st));
+    k_popc_total<<<grid_1d(n_blocks, kThreads) > 4096 ? 4096 : grid_1d(n_blocks), kThreads, 0, st>>>(
+        (const unsigned long long*)bitmaps, n_blocks, (unsigned long long*)tot);
+    RSH_LAUNCHED("k_popc_total");
+    int64_t h = 0;
+    RSH_CUDA(cudaMemcpyAsync(&h, tot, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RSH_CUDA(cudaStreamSynchronize(st));
+    if (h >= (1LL << 31)) return fail(kInvalid, "rsh_schedule: %lld tensor-core nonzeros exceed the 32-bit index limit", (long long)h);
+  }
   // uncovered rows
   if (n_rows) {
     RSH_CUDA(cudaMemsetAsync(s.uncov_flag, 1, n_rows, st));
@@ -1238,7 +1264,9 @@ int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bit
   Sched s;
   const size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_schedule_rowmajor: schedule buffer too small");
-  if (tc_nnz < 0 || !ulist || ulist_bytes < rsh_rowmajor_bytes(n_rows, n_entries, n_blocks, n_res, tc_nnz))
+  if (tc_nnz < 0 || tc_nnz >= (1LL << 31))
+    return fail(kInvalid, "rsh_schedule_rowmajor: %lld nonzeros exceed the 32-bit index limit", (long long)tc_nnz);
+  if (!ulist || ulist_bytes < rsh_rowmajor_bytes(n_rows, n_entries, n_blocks, n_res, tc_nnz))
     return fail(kInvalid, "rsh_schedule_rowmajor: list buffer smaller than rsh_rowmajor_bytes()");
   if ((uintptr_t)ulist & 15) return fail(kInvalid, "rsh_schedule_rowmajor: list must be 16-byte aligned");
   Carve cv(ulist);
@@ -1268,8 +1296,9 @@ int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bit
 }
 
 // bytes of chunk-partial workspace rsh_spmm needs (partial_slots from the schedule header)
-size_t rsh_partials_bytes(int64_t partial_slots, int64_t N, int32_t accum) {
-  return (size_t)(partial_slots > 0 ? partial_slots : 1) * 8 * (size_t)N * (accum ? sizeof(double) : sizeof(float));
+size_t rsh_partials_bytes(int64_t n_entries, int64_t partial_slots, int64_t N, int32_t accum) {
+  return spmm_ctl_bytes(n_entries) +
+         (size_t)(partial_slots > 0 ? partial_slots : 1) * 8 * (size_t)N * (accum ? sizeof(double) : sizeof(float));
 }
 
 // execute.py:155-218.  b_dtype: 0 f32, 1 bf16, 2 f16.  accum: 0 f32, 1 f64.  math: 0 = CUDA-core
@@ -1280,7 +1309,7 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum, void* sched, size_t sched_bytes,
                 void* partials, size_t partial_bytes, cudaStream_t st) {
   if (N < 1 || N > (1 << 30) || ldb < N || ldc < N || !B || !C) return fail(kInvalid, "rsh_spmm: bad dense operands");
-  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 16383) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
+  if (b_dtype < 0 || b_dtype > 2 || accum < 0 || accum > 32767) return fail(kInvalid, "rsh_spmm: bad dtype/accum");
   Sched s;
   size_t need = sched_layout(sched, n_rows, n_entries, n_blocks, n_res, &s);
   if (!sched || sched_bytes < need) return fail(kInvalid, "rsh_spmm: schedule buffer too small");
@@ -1300,10 +1329,12 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.N = (int32_t)N;
   a.window_size = window_size;
   a.s = s;
-  a.partials = partials;
+  a.N = (int32_t)N;
+  RSH_OK(bind_workspace(a, partials, partial_bytes, n_entries, (accum & 1) ? sizeof(double) : sizeof(float)));
   a.flags = accum >> 1;  // tuning knobs: bits 0-1 row-walk occupancy variant, bit 2 no L2 cache hints,
                          // bits 3-5 stream depth/occupancy variant, bit 6 row-walk kernel instead of the stream,
-                         // bit 8 stream gathers bypass L1 allocation, bit 10 list copies without L2 hint, bit 11 no lane groups, bit 12 ignore the row-major list
+                         // bit 8 stream gathers bypass L1 allocation, bit 10 list copies without L2 hint, bit 11 no lane groups, bit 12 ignore the row-major list,
+                         // bit 13 no window exceeds kTicketMax chunks (schedule header[6] == 0): skip the fix-up launches
   accum &= 1;
   // widest per-lane vector that tiles N and keeps loads aligned
   size_t esz = b_dtype == 0 ? 4 : 2;

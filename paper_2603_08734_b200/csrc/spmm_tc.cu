@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_spmm_tc(SpmmArgs a) {
   constexpr int SP = STAGES / kPipes;  // stages per pipeline
   static_assert(STAGES % kPipes == 0, "stages split evenly across pipelines");
   static_assert(SP >= 2, "at least double buffering per pipeline");
+  check_workspace(a);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                                   // STAGES * MT * 4 KB
@@ -665,7 +666,8 @@ int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
   a.N = (int32_t)N;
   a.window_size = window_size;
   a.s = s;
-  a.partials = partials;
+  a.N = (int32_t)N;
+  RSH_OK(bind_workspace(a, partials, partial_bytes, n_entries, sizeof(float)));
   a.flags = l1;
   l1 &= 1;
   const int mt = (int)(N / 128);

@@ -282,12 +282,29 @@ CHUNK_CC_LIST = int(os.environ.get("RSH_CC_LIST_CHUNK", "128"))
 CHUNK_TC = 256   # ... and for the tensor-core kernel (kChunkTC)
 
 
+def _tile_stamp(t: DeviceTile) -> tuple:
+    """Identity of a tile's arrays (address + torch version counter): a cached schedule and its
+    row-major list snapshot col_id / values, so they are rebuilt when an array is replaced or
+    modified in place."""
+    return tuple((getattr(t, f).data_ptr(), getattr(t, f)._version, getattr(t, f).numel()) for f in TILE_FIELDS)
+
+
 class SpmmPlan:
-    """Persistent-kernel work schedule of one DeviceTile for one unit size (built once, reused)."""
+    """Persistent-kernel work schedule of one DeviceTile for one unit size (built once, reused).
+
+    The schedule is read-only during SpMM launches; each launch's mutable state (work counter,
+    window tickets, chunk partials) lives in a workspace from ``workspace()``, one per (N,
+    accumulation, stream), so launches on different streams never share one."""
 
     def __init__(self, t: DeviceTile, chunk: int = CHUNK_CC, stream=None):
+        from .tile import FormatError, structural_issues
+        issues = structural_issues(t)
+        if issues:  # the kernels index with these arrays: refuse a malformed format up front
+            raise FormatError("; ".join(issues))
         dev = t.device
         self.chunk = chunk
+        self.stamp = _tile_stamp(t)
+        self.n_entries = t.n_entries
         self.nbytes = lib().rsh_schedule_bytes(t.n_rows, t.n_entries, t.n_blocks, t.n_res)
         self.buf = _ws(self.nbytes, dev)
         hdr = torch.zeros(8, dtype=torch.int64, device=dev)
@@ -296,7 +313,8 @@ class SpmmPlan:
              self.nbytes, _ptr(hdr), _stream(stream))
         h = hdr.cpu().tolist()
         self.groups, self.window_units, self.units, self.partial_slots, self.uncovered = h[:5]
-        self._partials = {}
+        self.fixup_windows = h[6]
+        self._ws = {}
         self.ulist = None
         if chunk == CHUNK_CC_LIST:
             # the streaming kernel's pre-decoded window list (8 bytes per tc nonzero)
@@ -307,29 +325,36 @@ class SpmmPlan:
                  t.n_blocks, tc_nnz, t.n_res, _ptr(self.buf), self.nbytes, _ptr(self.ulist), 8 * self.ulist.numel(),
                  _stream(stream))
 
-    def partials(self, N: int, accum: int, dev) -> torch.Tensor:
-        key = (N, accum)
-        if key not in self._partials:
-            nbytes = lib().rsh_partials_bytes(self.partial_slots, N, accum)
-            self._partials[key] = _ws(nbytes, dev)
-        return self._partials[key]
+    def workspace(self, N: int, accum: int, dev, stream=None) -> torch.Tensor:
+        """Zero-filled SpMM workspace (control block + chunk partials) for one stream."""
+        sid = _stream(stream)
+        key = (N, accum, sid)
+        if key not in self._ws:
+            nbytes = lib().rsh_partials_bytes(self.n_entries, self.partial_slots, N, accum)
+            self._ws[key] = torch.zeros(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
+        return self._ws[key]
+
+    partials = workspace  # round-1 name
 
 
 # the streaming kernel reads a pre-decoded row-major window list (rsh_schedule_rowmajor)
 ROWMAJOR_LIST = os.environ.get("RSH_ROWMAJOR_LIST", "1") != "0"
 # rsh_spmm_cc tuning knobs (accum bits 1..): development override through RSH_CC_VARIANT
 CC_VARIANT = int(os.environ.get("RSH_CC_VARIANT", "0"))
+NO_FIXUP = 8192  # cc variant bit: the schedule has no window the fix-up kernels must reduce
 
 
 def spmm_plan(t: DeviceTile, chunk: int = CHUNK_CC) -> SpmmPlan:
-    """The cached schedule of ``t`` for units of ``chunk`` blocks."""
+    """The cached schedule of ``t`` for units of ``chunk`` blocks (rebuilt when the tile's arrays
+    were replaced or modified in place since it was built)."""
     if t._plan is None:
         t._plan = {}
     elif isinstance(t._plan, SpmmPlan):  # a single prebuilt schedule handed over by a caller
         t._plan = {t._plan.chunk: t._plan}
-    if chunk not in t._plan:
-        t._plan[chunk] = SpmmPlan(t, chunk)
-    return t._plan[chunk]
+    pl = t._plan.get(chunk)
+    if pl is None or pl.stamp != _tile_stamp(t):
+        pl = t._plan[chunk] = SpmmPlan(t, chunk)
+    return pl
 
 
 def tc_eligible(t: DeviceTile, b: torch.Tensor, accumulate: str = "f32") -> bool:
@@ -385,11 +410,14 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
     else:
         chunk = CHUNK_CC
     plan = spmm_plan(t, chunk)
-    part = plan.partials(N, acc, b.device)
+    part = plan.workspace(N, acc, b.device, stream)
+    flags = int(l1) if path == "tc" else acc | (cc_variant << 1)
+    if plan.fixup_windows == 0:
+        flags |= NO_FIXUP << 1 if path != "tc" else NO_FIXUP
     call("rsh_spmm_tc" if path == "tc" else "rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
          _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),
          _ptr(t.res_values), t.n_res, _ptr(b), b.stride(0), _BDT[b.dtype], N, _ptr(out), out.stride(0),
-         int(l1) if path == "tc" else acc | (cc_variant << 1), _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
+         flags, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
     return out
 
 

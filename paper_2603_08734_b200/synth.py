@@ -1,14 +1,16 @@
-"""Seeded synthetic inputs: the five BASELINE.json workloads and the reference's power-law corpus.
+"""Seeded synthetic inputs: the five BASELINE.json workloads (bench and parity-test inputs).
 
 Recipes follow SURVEY.md Appendix B exactly (same numpy Generator call sequence), so the
 counts quoted there reproduce: config 2 -> nnz 16,086,387, 546,921 touched columns, etc.
-``generate_power_law`` reproduces the reference generator (core.py:300-373) draw for draw so
-the reference test corpora (conftest.py:22-45, test_acceptance.py:62-89) can be rebuilt on a
-machine without the reference installed.
+``rmat_sNN`` names the weak-scaling R-MAT graphs (scale NN, edge factor 16, seed 0) of the
+multi-GPU run.  The reference's power-law test corpus lives in oracle/corpus.py (test
+infrastructure).
 """
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -25,25 +27,65 @@ def _csr_from_keys(n_rows: int, n_cols: int, keys: np.ndarray, values: np.ndarra
     return CsrMatrix(n_rows, n_cols, rp, cols, values)
 
 
-def rmat_keys(scale: int, edge_factor: int, rng: np.random.Generator, a=0.57, b=0.19, c=0.19) -> np.ndarray:
-    """R-MAT edge keys (row * n + col), deduplicated and sorted."""
+def sorted_unique(x: np.ndarray) -> np.ndarray:
+    """np.unique for a 1-D integer array (sort + adjacent-difference mask: numpy 2.3's
+    np.unique is ~50x slower on 10^7 int64 keys)."""
+    x = np.sort(x)
+    if x.size < 2:
+        return x
+    keep = np.empty(x.size, dtype=bool)
+    keep[0] = True
+    np.not_equal(x[1:], x[:-1], out=keep[1:])
+    return x[keep]
+
+
+def _threads() -> int:
+    return max(1, min(16, len(os.sched_getaffinity(0))))
+
+
+def rmat_keys(scale: int, edge_factor: int, seed: int, a=0.57, b=0.19, c=0.19) -> tuple[np.ndarray, np.random.Generator]:
+    """R-MAT edge keys (row * n + col), deduplicated and sorted, and the generator positioned
+    after the draws.  The recipe draws ``u = rng.random(m)`` once per
+    bit from ``default_rng(seed)`` and sets row bit (u >= a+b), column bit ((a <= u < a+b) or
+    u >= a+b+c).  The same stream is produced here in parallel: PCG64 advances in O(log n), so
+    each thread draws its slice [lo, hi) of every bit's m doubles from a copy advanced to
+    bit * m + lo (Generator.random consumes one 64-bit output per double)."""
     n = 1 << scale
     m = edge_factor * n
     r = np.zeros(m, dtype=np.int64)
     q = np.zeros(m, dtype=np.int64)
-    for bit in range(scale):
-        u = rng.random(m)
-        down = u >= a + b
-        right = ((u >= a) & (u < a + b)) | (u >= a + b + c)
-        r |= down.astype(np.int64) << bit
-        q |= right.astype(np.int64) << bit
-        del u, down, right
-    return np.unique(r * n + q)
+    nt = _threads()
+    cuts = [m * i // nt for i in range(nt + 1)]
+    ta, tab, tabc = a, a + b, a + b + c
+
+    def work(i):
+        lo, hi = cuts[i], cuts[i + 1]
+        if hi <= lo:
+            return
+        rs, qs = r[lo:hi], q[lo:hi]
+        for bit in range(scale):
+            g = np.random.Generator(np.random.PCG64(seed).advance(bit * m + lo))
+            u = g.random(hi - lo)
+            # category (u >= a) + (u >= a+b) + (u >= a+b+c): row bit = cat >= 2, column bit = cat odd
+            cat = (u >= ta).view(np.uint8)
+            cat += (u >= tab).view(np.uint8)
+            cat += (u >= tabc).view(np.uint8)
+            del u
+            rs |= (cat >> 1).astype(np.int64) << bit
+            qs |= (cat & 1).astype(np.int64) << bit
+
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(work, range(nt)))
+    keys = r
+    keys *= n
+    keys += q
+    del q
+    rng = np.random.Generator(np.random.PCG64(seed).advance(scale * m))
+    return sorted_unique(keys), rng
 
 
 def rmat(scale: int, edge_factor: int, seed: int) -> CsrMatrix:
-    rng = np.random.default_rng(seed)
-    keys = rmat_keys(scale, edge_factor, rng)
+    keys, rng = rmat_keys(scale, edge_factor, seed)
     n = 1 << scale
     vals = rng.uniform(-1.0, 1.0, keys.size).astype(np.float32)
     return _csr_from_keys(n, n, keys, vals)
@@ -85,11 +127,11 @@ def bf16_round(x: np.ndarray) -> np.ndarray:
 def heavy_tail_4m() -> CsrMatrix:
     scale = 22
     n = 1 << scale
-    keys = rmat_keys(scale, 16, np.random.default_rng(0))
+    keys, _ = rmat_keys(scale, 16, 0)
     rng1 = np.random.default_rng(1)
     dense = np.sort(rng1.choice(n, 8, replace=False))
     extra = np.concatenate([r * n + rng1.choice(n, n // 4, replace=False) for r in dense])
-    keys = np.union1d(keys, extra)
+    keys = sorted_unique(np.concatenate([keys, extra]))  # np.union1d
     vals = bf16_round(np.random.default_rng(2).uniform(-1.0, 1.0, keys.size).astype(np.float32))
     return _csr_from_keys(n, n, keys, vals)
 
@@ -112,7 +154,19 @@ WORKLOADS = {
 }
 
 
+def workload_spec(name: str) -> Workload:
+    """WORKLOADS[name], plus ``rmat_sNN`` (R-MAT scale NN, ef16, N=128, fp32)."""
+    if name in WORKLOADS:
+        return WORKLOADS[name]
+    if name.startswith("rmat_s") and name[6:].isdigit():
+        s = int(name[6:])
+        return Workload(name, f"R-MAT scale {s} ef16, N=128, fp32", 128, "f32", 1)
+    raise KeyError(name)
+
+
 def workload_matrix(name: str) -> CsrMatrix:
+    if name.startswith("rmat_s") and name[6:].isdigit():
+        return rmat(int(name[6:]), 16, 0)
     if name == "uniform4k":
         return uniform_4096()
     if name == "rmat1m":
@@ -129,134 +183,8 @@ def workload_matrix(name: str) -> CsrMatrix:
 def workload_b(name: str, n_rows: int, rows=None) -> np.ndarray:
     """B = uniform(-1, 1, (n, N)) from default_rng(b_seed); bf16 workloads are rounded to bf16.
     ``rows`` restricts generation to a prefix (the full draw is made, as the recipe does)."""
-    w = WORKLOADS[name]
+    w = workload_spec(name)
     b = np.random.default_rng(w.b_seed).uniform(-1.0, 1.0, (n_rows, w.n_features)).astype(np.float32)
     if w.dtype == "bf16":
         b = bf16_round(b)
     return b
-
-
-# ---------------------------------------------------------------------------------------------
-# the reference's power-law generator (core.py:300-373), reproduced draw for draw
-# ---------------------------------------------------------------------------------------------
-
-_SCATTER_NNZ = 1      # rows with <= this many nonzeros scatter over all columns
-_ROWS_PER_COMMUNITY = 8
-_POOL_SCALE = 1.5
-
-
-def _scaled_counts(raw: np.ndarray, target: int, cap: int) -> np.ndarray:
-    """Smallest scale (by 80-step bisection after doubling) whose clipped rounded counts reach
-    the target; returns those counts."""
-    if target == 0:
-        return np.zeros(raw.size, dtype=np.int64)
-
-    def at(scale):
-        return np.minimum(np.rint(raw * scale), cap)
-
-    hi = 1.0
-    while at(hi).sum() < target and hi < 1e18:
-        hi *= 2.0
-    lo = 0.0
-    for _ in range(80):
-        mid = (lo + hi) / 2
-        if at(mid).sum() >= target:
-            hi = mid
-        else:
-            lo = mid
-    return at(hi).astype(np.int64)
-
-
-def _interleave_gaps(counts: np.ndarray) -> np.ndarray:
-    """Runs of 8 long rows (draw order) alternating with evenly cut bursts of short rows."""
-    long_rows = counts[counts > _SCATTER_NNZ]
-    short_rows = counts[counts <= _SCATTER_NNZ]
-    if long_rows.size == 0 or short_rows.size == 0:
-        return counts
-    groups = -(-long_rows.size // _ROWS_PER_COMMUNITY)
-    edges = np.round(np.linspace(0, short_rows.size, groups + 1)).astype(np.int64)
-    parts = []
-    for g in range(groups):
-        parts.append(long_rows[g * _ROWS_PER_COMMUNITY:(g + 1) * _ROWS_PER_COMMUNITY])
-        parts.append(short_rows[edges[g]:edges[g + 1]])
-    return np.concatenate(parts)
-
-
-def generate_power_law(n_rows: int, n_cols: int, target_nnz: int, skew: float, seed: int) -> CsrMatrix:
-    if skew <= 0:
-        raise ValueError("skew must be positive")
-    if target_nnz < 0 or target_nnz > n_rows * n_cols:
-        raise ValueError("target_nnz infeasible for the given dimensions")
-    rng = np.random.default_rng(seed)
-    if 0 in (n_rows, n_cols, target_nnz):
-        return CsrMatrix(n_rows, n_cols, np.zeros(n_rows + 1, np.int64), np.empty(0), np.empty(0))
-    counts = _interleave_gaps(_scaled_counts(rng.pareto(skew, n_rows) + 1.0, target_nnz, n_cols))
-    is_long = counts > _SCATTER_NNZ
-    n_long = int(is_long.sum())
-    if n_long:
-        comm = np.zeros(n_rows, dtype=np.int64)
-        comm[is_long] = np.arange(n_long) // _ROWS_PER_COMMUNITY
-        n_comm = int(comm[is_long].max()) + 1
-        pool = int(min(n_cols, max(16, round(_POOL_SCALE * _ROWS_PER_COMMUNITY * float(counts[is_long].mean())))))
-        spread = n_cols - pool
-        if n_comm > 1:
-            origin = np.round(np.arange(n_comm) * spread / max(1, n_comm - 1)).astype(np.int64)
-        else:
-            origin = np.zeros(1, dtype=np.int64)
-    everything = np.arange(n_cols)
-    per_row = []
-    for r in range(n_rows):
-        k = int(counts[r])
-        if k == 0:
-            per_row.append(np.empty(0, dtype=np.int64))
-        elif k <= _SCATTER_NNZ:
-            per_row.append(np.sort(rng.choice(n_cols, size=k, replace=False)))
-        else:
-            o = int(origin[comm[r]])
-            window = np.arange(o, o + pool)
-            if k <= pool:
-                picked = rng.choice(window, size=k, replace=False)
-            else:
-                outside = np.concatenate([everything[:o], everything[o + pool:]])
-                picked = np.concatenate([window, rng.choice(outside, size=k - pool, replace=False)])
-            per_row.append(np.sort(picked))
-    cols = np.concatenate(per_row)
-    rp = np.zeros(n_rows + 1, dtype=np.int64)
-    np.cumsum(counts, out=rp[1:])
-    vals = rng.uniform(-1.0, 1.0, size=cols.size).astype(np.float32)
-    return CsrMatrix(n_rows, n_cols, rp, cols, vals)
-
-
-def small_corpus() -> list[CsrMatrix]:
-    """The reference's 24-matrix fixture (conftest.py:22-45)."""
-    out, i = [], 0
-    for n in (32, 48, 64, 96, 128, 192):
-        for delta in (0, 1):
-            n_cols = n if delta == 0 else max(16, n // 2)
-            dens = (0.01, 0.03, 0.08)[(i + delta) % 3]
-            out.append(generate_power_law(n, n_cols, max(1, int(round(dens * n * n_cols))),
-                                          (1.2, 1.5, 2.0)[i % 3], seed=100 + i))
-            i += 1
-        for delta in (2, 3):
-            n_cols = min(256, 2 * n) if delta == 2 else n
-            dens = (0.01, 0.03, 0.08)[i % 3]
-            out.append(generate_power_law(n, n_cols, max(1, int(round(dens * n * n_cols))),
-                                          (1.2, 1.5, 2.0)[(i + 1) % 3], seed=200 + i))
-            i += 1
-    return out
-
-
-def acceptance_cases() -> list[tuple]:
-    """(n_rows, n_cols, nnz, skew, seed, d) of the reference acceptance corpus
-    (test_acceptance.py:62-89)."""
-    rng = np.random.default_rng(990099)
-    sizes = [64, 96, 128, 192, 256, 384, 512]
-    rows = [sizes[i % 7] for i in range(150)] + [768 if i % 2 else 1024 for i in range(40)]
-    rows += [2048] * 8 + [4096] * 2
-    cases = []
-    for i, nr in enumerate(rows):
-        nc = 3 * nr // 4 if i % 4 == 1 else (2 * nr if i % 7 == 3 else nr)
-        dens = 10 ** rng.uniform(-3.0, -1.0)
-        nnz = max(16, min(int(round(dens * nr * nc)), 150_000, int(0.4 * nr * nc)))
-        cases.append((nr, nc, nnz, (1.2, 1.5, 2.0)[i % 3], i, (16, 64, 128)[i % 3]))
-    return cases

@@ -176,6 +176,43 @@ def _report(t, res_ok: bool, check_bits: bool, check_cover: bool) -> np.ndarray:
     return rep.cpu().numpy()
 
 
+def structural_issues(t) -> list[str]:
+    """The subset of validate_rstile's checks the SpMM kernels rely on for memory safety (array
+    lengths, offsets monotone and in bounds, row / column ids in range, popcount sum = value
+    count).  One device pass; the schedule build refuses a format that fails any of them (the
+    reference executor would raise IndexError / FormatError or read garbage from numpy arrays
+    on such input, never write out of bounds)."""
+    E, nb, R = t.n_entries, t.n_blocks, t.n_res
+    if not (1 <= t.window_size <= 8):
+        return [f"window_size {t.window_size} outside 1..8"]
+    if t.row_window_offset.numel() != E + 1:
+        return ["row_window_offset length must be entries + 1"]
+    if t.res_offset.numel() != R + 1:
+        return ["residual offset length must be rows + 1"]
+    if t.col_id.numel() != nb * 8:
+        return ["col_id length must be 8 per block"]
+    r = _report(t, True, False, False)
+    out: list[str] = []
+    if r[_OFF0] != 0 or r[_OFF_NONMONO] != _NONE or r[_OFF_LAST] != nb:
+        out.append("row_window_offset must run monotonically from 0 to the block count")
+    if t.col_id.numel() and (r[_COL_MIN] < 0 or r[_COL_MAX] >= t.n_cols):
+        out.append("col_id entry out of range")
+    if E and (r[_RWID_MIN] < 0 or r[_RWID_MAX] >= t.n_rows):
+        out.append("row_window_id out of range")
+    if r[_POP_SUM] != t.values.numel():
+        out.append(f"bitmap popcount sum {int(r[_POP_SUM])} does not match value count {t.values.numel()}")
+    if r[_ROFF0] != 0 or r[_ROFF_NONMONO] != _NONE or r[_ROFF_LAST] != t.res_values.numel() \
+            or t.res_col_id.numel() != t.res_values.numel():
+        out.append("residual offsets must run monotonically from 0 to the residual entry count")
+    if R and (r[_RROW_MIN] < 0 or r[_RROW_MAX] >= t.n_rows):
+        out.append("residual row_id out of range")
+    if t.res_col_id.numel() and (r[_RCOL_MIN] < 0 or r[_RCOL_MAX] >= t.n_cols):
+        out.append("residual col_id out of range")
+    if t.values.numel() >= 2 ** 31 or t.res_values.numel() >= 2 ** 31:
+        out.append("more than 2^31 - 1 nonzeros in one part (int32 value offsets)")
+    return out
+
+
 def validate_rstile_device(t) -> list[str]:
     """tile.py:176-267 for a DeviceTile: every structural invariant, checked on device; an empty
     list means valid.  Messages and their order are the reference's."""

@@ -31,7 +31,8 @@ def known_answers():
 @pytest.fixture(scope="session")
 def small_corpus():
     from paper_2603_08734_b200 import synth
-    return synth.small_corpus()
+    from oracle import corpus  # noqa: E402
+    return corpus.small_corpus()
 
 
 @pytest.fixture(scope="session")

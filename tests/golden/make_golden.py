@@ -31,6 +31,8 @@ from rstile import core, partition, tile  # noqa: E402
 
 from paper_2603_08734_b200 import synth  # noqa: E402
 
+from oracle import corpus  # noqa: E402
+
 PARAM_SETS = {
     "default": {},
     "tc_only": {"tau_nnz": 0},
@@ -92,12 +94,12 @@ def format_record(a, params: dict) -> dict:
 def corpus_matrices():
     """name -> (recipe, CsrMatrix) for every corpus the digests cover."""
     out = {}
-    for i, a in enumerate(synth.small_corpus()):
+    for i, a in enumerate(corpus.small_corpus()):
         out[f"small{i:02d}"] = ({"kind": "small_corpus", "index": i}, a)
-    for j, (nr, nc, nnz, skew, seed, _d) in enumerate(synth.acceptance_cases()):
+    for j, (nr, nc, nnz, skew, seed, _d) in enumerate(corpus.acceptance_cases()):
         if j % 4 == 0 or nr >= 2048:  # a quarter of the 200-matrix corpus plus all large ones
             out[f"accept{j:03d}"] = ({"kind": "power_law", "args": [nr, nc, nnz, skew, seed]},
-                                     synth.generate_power_law(nr, nc, nnz, skew, seed))
+                                     corpus.generate_power_law(nr, nc, nnz, skew, seed))
     for s in (12, 14, 16):
         out[f"rmat{s}"] = ({"kind": "rmat", "args": [s, 16, 0]}, synth.rmat(s, 16, 0))
     return out
@@ -198,7 +200,7 @@ def main() -> None:
     with open(os.path.join(HERE, "known_answers.json"), "w") as fh:
         json.dump(known_answers(), fh)
     spmm = {}
-    for i, a in enumerate(synth.small_corpus()):
+    for i, a in enumerate(corpus.small_corpus()):
         ref_a = core.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
         b = np.random.default_rng(a.nnz).uniform(-1, 1, (a.n_cols, 16)).astype(np.float32)
         spmm[f"c{i:02d}"] = core.oracle_spmm(ref_a, core.DenseMatrix.from_array(b)).data

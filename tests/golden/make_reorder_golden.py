@@ -23,6 +23,8 @@ from rstile.core import CsrMatrix as RefCsr  # noqa: E402
 
 from paper_2603_08734_b200 import synth  # noqa: E402
 
+from oracle import corpus  # noqa: E402
+
 CASES = [
     ("small3", {"kind": "small_corpus", "index": 3}),
     ("small8", {"kind": "small_corpus", "index": 8}),
@@ -38,12 +40,12 @@ def matrix(recipe, small):
     if recipe["kind"] == "small_corpus":
         return small[recipe["index"]]
     if recipe["kind"] == "power_law":
-        return synth.generate_power_law(*recipe["args"])
+        return corpus.generate_power_law(*recipe["args"])
     return synth.rmat(*recipe["args"])
 
 
 def main():
-    small = synth.small_corpus()
+    small = corpus.small_corpus()
     out = []
     for name, recipe in CASES:
         a = matrix(recipe, small)

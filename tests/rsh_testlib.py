@@ -26,10 +26,11 @@ def digest(*arrays) -> str:
 
 def corpus_matrix(recipe: dict, small=None):
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     if recipe["kind"] == "small_corpus":
-        return (small or synth.small_corpus())[recipe["index"]]
+        return (small or corpus.small_corpus())[recipe["index"]]
     if recipe["kind"] == "power_law":
-        return synth.generate_power_law(*recipe["args"])
+        return corpus.generate_power_law(*recipe["args"])
     if recipe["kind"] == "rmat":
         return synth.rmat(*recipe["args"])
     raise KeyError(recipe["kind"])

@@ -23,5 +23,6 @@ def test_reference_arm_prints_one_json_line():
                 "config", "cpu_baseline", "e2e"):
         assert key in rec, key
     assert rec["value"] > 0 and rec["warmup"] >= 3
-    assert rec["cpu_baseline"]["kind"] == "port" and rec["cpu_baseline"]["cores"] >= 1
+    assert rec["cpu_baseline"]["kind"] in ("reference", "port") and rec["cpu_baseline"]["cores"] >= 1
+    assert rec["config"]["workload"] == "uniform4k"
     assert rec["e2e"]["h2d_bytes_per_step"] == 0

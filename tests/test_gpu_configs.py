@@ -1,9 +1,11 @@
-"""GPU: the BASELINE.json workloads at full size (configs 1-4; config 5 with RSH_FULL_CONFIGS=1).
+"""GPU: the five BASELINE.json workloads at full size (config 5 = R-MAT scale 24, 263,433,540 nnz).
 
 Per config:
 * the device-built RS-Tile (partition + split + build, on device) is bit-exact with the CPU
   oracle's build of the same matrix (the oracle itself is pinned to the reference by
-  tests/test_oracle_golden.py);
+  tests/test_oracle_golden.py), and -- for the configs whose reference build fits this
+  container (tests/golden/make_config_golden.py) -- with SHA-256 digests of the REFERENCE's
+  own build of the same matrix;
 * C from the exact-FP32 CUDA-core path matches the f64 oracle to the reference's 1e-5
   max-relative gate (excluding the long-row reductions the reference's own f32 path fails,
   SURVEY.md 8(c)) and 1e-6 relative Frobenius on sampled row ranges;
@@ -15,20 +17,28 @@ Per config:
 
 from __future__ import annotations
 
+import json
 import os
 
 import numpy as np
 import pytest
 
 import oracle as O
+from rsh_testlib import GOLDEN, digest
 
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
 
-CONFIGS = ["uniform4k", "rmat1m", "stencil2m", "heavytail4m"]
-if os.environ.get("RSH_FULL_CONFIGS") == "1":
-    CONFIGS.append("rmat16m")
+CONFIGS = ["uniform4k", "rmat1m", "stencil2m", "heavytail4m", "rmat16m"]
+
+
+def _reference_digests():
+    try:
+        with open(os.path.join(GOLDEN, "config_formats.json")) as fh:
+            return json.load(fh)["configs"]
+    except OSError:
+        return {}
 
 
 def _sample_ranges(n_rows: int, k: int = 6, width: int = 4096, seed: int = 0):
@@ -45,12 +55,26 @@ def config(request):
     from paper_2603_08734_b200.device import DeviceCsr, build_device
     name = request.param
     a = synth.workload_matrix(name)
-    w = synth.WORKLOADS[name]
+    w = synth.workload_spec(name)
     b = synth.workload_b(name, a.n_cols)
     t = build_device(DeviceCsr.from_host(a))
     yield name, w, a, b, t
     del t
     torch.cuda.empty_cache()
+
+
+def test_format_digests_match_reference_build(config):
+    """Full-size pin: the device format equals the reference's own build, array by array."""
+    name, _, a, _, t = config
+    ref = _reference_digests().get(name)
+    if ref is None:
+        pytest.skip(f"no reference build recorded for {name} (tests/golden/make_config_golden.py)")
+    assert ref["input"] == digest(np.array([a.n_rows, a.n_cols]), a.row_ptr, a.col_idx, a.values), name
+    h = t.host_arrays()
+    f = ref["format"]
+    assert (t.n_entries, t.n_blocks, t.window_size) == (f["n_entries"], f["n_blocks"], f["window_size"])
+    for k, want in f["arrays"].items():
+        assert digest(h[k]) == want, (name, k)
 
 
 def test_format_bit_exact_with_oracle(config):

@@ -56,7 +56,8 @@ def test_exec_tc_window_identity_and_dense():
     with pytest.raises(IndexError):
         P.exec_tc_window(m, 1, b, c)
     from paper_2603_08734_b200 import synth
-    a = synth.generate_power_law(8, 16, 50, 1.5, seed=3)
+    from oracle import corpus  # noqa: E402
+    a = corpus.generate_power_law(8, 16, 50, 1.5, seed=3)
     m = _build(a, force_tc)
     assert m.tc.n_entries == 1 and m.residual.n_rows == 0
     b = _b(16, 7, 3)

@@ -20,9 +20,10 @@ def _dense(a) -> np.ndarray:
 @pytest.mark.parametrize("shape", [(700, 500, 9000), (1500, 1500, 30000), (64, 3000, 4000)])
 def test_transpose_is_canonical_and_exact(shape):
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import DeviceCsr
     from paper_2603_08734_b200.gnn import transpose_device
-    a = synth.generate_power_law(*shape, 1.5, seed=11)
+    a = corpus.generate_power_law(*shape, 1.5, seed=11)
     t = transpose_device(DeviceCsr.from_host(a))
     rp, ci, va = t.row_ptr.cpu().numpy(), t.col_idx.cpu().numpy(), t.values.cpu().numpy()
     assert t.n_rows == a.n_cols and t.n_cols == a.n_rows
@@ -38,8 +39,9 @@ def test_transpose_is_canonical_and_exact(shape):
 @pytest.mark.parametrize("n_feat", [32, 64, 128])
 def test_forward_backward_against_dense(n_feat):
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.gnn import SparseOperator
-    a = synth.generate_power_law(1200, 900, 20000, 1.5, seed=5)
+    a = corpus.generate_power_law(1200, 900, 20000, 1.5, seed=5)
     op = SparseOperator.from_csr(a)
     g = torch.Generator().manual_seed(0)
     h = torch.rand((a.n_cols, n_feat), generator=g).mul_(2).sub_(1).cuda().requires_grad_(True)
@@ -56,8 +58,9 @@ def test_forward_backward_against_dense(n_feat):
 
 def test_gcn_layer_trains():
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.gnn import GCNLayer, SparseOperator
-    a = synth.generate_power_law(800, 800, 12000, 1.4, seed=2)
+    a = corpus.generate_power_law(800, 800, 12000, 1.4, seed=2)
     op = SparseOperator.from_csr(a)
     torch.manual_seed(0)
     layer = GCNLayer(op, 16, 8).cuda()
@@ -84,8 +87,9 @@ def test_gcn_layer_trains():
 
 def test_shape_errors():
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.gnn import SparseOperator
-    a = synth.generate_power_law(100, 80, 600, 1.5, seed=1)
+    a = corpus.generate_power_law(100, 80, 600, 1.5, seed=1)
     op = SparseOperator.from_csr(a)
     with pytest.raises(ValueError):
         op(torch.zeros((81, 4), device="cuda"))

@@ -207,7 +207,7 @@ def test_cancellation_f32_fails_check_f64_exact():
 @pytest.mark.parametrize("precision", ["f32", "f64"])
 def test_split_granularity_is_bitwise_invisible(precision):
     a = P.CsrMatrix(*(lambda x: (x.n_rows, x.n_cols, x.row_ptr, x.col_idx, x.values))(
-        __import__("paper_2603_08734_b200.synth", fromlist=["x"]).generate_power_law(128, 512, 4000, 2.0, seed=11)))
+        __import__("oracle.corpus", fromlist=["x"]).generate_power_law(128, 512, 4000, 2.0, seed=11)))
     b = P.DenseMatrix.from_array(rand_b(512, 16, 11))
     cfg = P.ExecConfig(accumulate_precision=precision)
     blobs = {P.hybrid_spmm(build(a, P.PartitionParams(max_blocks_per_item=k)), b, cfg).data.tobytes()
@@ -234,7 +234,8 @@ def test_long_window_multi_chunk_reduction():
 @pytest.mark.parametrize("d", [1, 3, 5, 7, 32, 33, 96, 128, 256, 384])
 def test_feature_widths(d):
     from paper_2603_08734_b200 import synth
-    a = synth.generate_power_law(300, 200, 3000, 1.5, seed=d)
+    from oracle import corpus  # noqa: E402
+    a = corpus.generate_power_law(300, 200, 3000, 1.5, seed=d)
     m = build(a)
     b = rand_b(200, d, d)
     ref, _ = O.spmm_f64(O.Csr.of(a), b)
@@ -245,8 +246,9 @@ def test_feature_widths(d):
 def test_half_precision_b(dt):
     import torch
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import DeviceCsr, build_device, spmm_device
-    a = synth.generate_power_law(512, 400, 8000, 1.5, seed=5)
+    a = corpus.generate_power_law(512, 400, 8000, 1.5, seed=5)
     t = build_device(DeviceCsr.from_host(a))
     b = torch.from_numpy(rand_b(400, 256, 1)).cuda().to(getattr(torch, dt))
     c = spmm_device(t, b, math="fp32")  # CUDA-core path: half B, fp32 A values, exact products
@@ -257,8 +259,9 @@ def test_half_precision_b(dt):
 def test_device_api_out_buffer_and_errors():
     import torch
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import DeviceCsr, build_device
-    a = synth.generate_power_law(256, 128, 2000, 1.5, seed=2)
+    a = corpus.generate_power_law(256, 128, 2000, 1.5, seed=2)
     t = build_device(DeviceCsr.from_host(a))
     b = torch.from_numpy(rand_b(128, 64, 2)).cuda()
     out = torch.full((256, 64), float("nan"), device="cuda")
@@ -296,8 +299,9 @@ def test_stream_kernel_bit_identical_across_variants(dtype):
     including multi-chunk windows (partials + ticket / fix-up reduction) and a near-dense row."""
     import torch
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import DeviceCsr, build_device, spmm_device
-    a = synth.generate_power_law(3000, 2500, 60000, 1.3, seed=21)
+    a = corpus.generate_power_law(3000, 2500, 60000, 1.3, seed=21)
     dense = np.zeros((a.n_rows, a.n_cols), np.float32)
     rows = np.repeat(np.arange(a.n_rows), np.diff(np.asarray(a.row_ptr)))
     dense[rows, np.asarray(a.col_idx)] = np.asarray(a.values)

@@ -52,8 +52,9 @@ def test_tf32_matches_fp64_oracle(small_corpus, d):
 @pytest.mark.parametrize("d", [128, 256])
 def test_half_operands_on_tensor_cores(dt, d):
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import resolve_math, spmm_device
-    a = synth.generate_power_law(700, 500, 9000, 1.5, seed=3)
+    a = corpus.generate_power_law(700, 500, 9000, 1.5, seed=3)
     t = _tile(a)
     b = _b(500, d, 5, getattr(torch, dt))
     assert resolve_math("auto", b, t, "f32") == "cc"  # the streaming CUDA-core kernel is faster
@@ -71,8 +72,9 @@ def test_tf32_rounding_is_not_truncation():
     """A values are rounded to tf32 with cvt.rna before the MMA; with a bf16-exact A and B the
     TF32 product is exact."""
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import spmm_device
-    a = synth.generate_power_law(256, 256, 4000, 1.5, seed=9)
+    a = corpus.generate_power_law(256, 256, 4000, 1.5, seed=9)
     vals = synth.bf16_round(np.asarray(a.values))
     a = P.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, vals)
     t = _tile(a)
@@ -85,8 +87,9 @@ def test_tf32_rounding_is_not_truncation():
 @pytest.mark.parametrize("l1", [True, False])
 def test_tc_split_invariance_and_determinism(l1):
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import spmm_device
-    a = synth.generate_power_law(128, 4096, 40000, 2.0, seed=11)
+    a = corpus.generate_power_law(128, 4096, 40000, 2.0, seed=11)
     b = _b(4096, 128, 11)
     outs = set()
     for k in (1, 4, 64, None):

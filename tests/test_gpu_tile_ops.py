@@ -91,8 +91,9 @@ def test_round_trip_small_corpus(kw):
     from paper_2603_08734_b200 import (PartitionParams, build_rstile, csr_equal, decode_rstile,
                                        partition_rows, split_long_work, validate_rstile)
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     p = PartitionParams(**kw)
-    for a in synth.small_corpus():
+    for a in corpus.small_corpus():
         m = build_rstile(a, split_long_work(a, partition_rows(a, p), p))
         assert validate_rstile(m) == []
         assert csr_equal(decode_rstile(m), a)
@@ -103,6 +104,7 @@ def test_round_trip_full_size_on_device(name):
     """decode(build(A)) == A bit-exactly at the benchmark sizes, device resident throughout."""
     import torch
     from paper_2603_08734_b200 import synth
+    from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import DeviceCsr, build_device
     from paper_2603_08734_b200.tile import decode_rstile_device, validate_rstile_device
     a = synth.workload_matrix(name)

@@ -44,8 +44,10 @@ def test_workspace_queries_are_pure_host_calls():
     a = L.rsh_schedule_bytes(1000, 100, 1000, 10)
     b = L.rsh_schedule_bytes(2000, 100, 1000, 10)
     assert b > a > 0
-    assert L.rsh_partials_bytes(10, 128, 0) == 10 * 8 * 128 * 4
-    assert L.rsh_partials_bytes(10, 128, 1) == 10 * 8 * 128 * 8
+    # control block (4 words + one ticket per entry, 256-byte aligned) + the chunk partials
+    assert L.rsh_partials_bytes(100, 10, 128, 0) == 512 + 10 * 8 * 128 * 4
+    assert L.rsh_partials_bytes(100, 10, 128, 1) == 512 + 10 * 8 * 128 * 8
+    assert L.rsh_partials_bytes(0, 10, 64, 0) == 256 + 10 * 8 * 64 * 4
 
 
 def test_library_is_built_for_sm100a():

@@ -5,9 +5,10 @@ import numpy as np, torch
 import oracle as O
 import paper_2603_08734_b200 as P
 from paper_2603_08734_b200 import synth
+from oracle import corpus  # noqa: E402
 from paper_2603_08734_b200.device import DeviceCsr, build_device, spmm_device
 
-a = synth.generate_power_law(2048, 1536, 30000, 1.5, seed=1)
+a = corpus.generate_power_law(2048, 1536, 30000, 1.5, seed=1)
 t = build_device(DeviceCsr.from_host(a))
 b = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, (a.n_cols, 128)).astype(np.float32)).cuda()
 ref32, ref64 = O.spmm_f64(O.Csr.of(a), b.cpu().numpy())

@@ -162,15 +162,29 @@ int rsh_spmm_cc(int64_t n_rows, int32_t window_size, int64_t n_entries, const ui
                 const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t accum,
                 void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
 
+/* rsh_tc_fragments: schedule-time image of every 8x8 block in the MMA's shared-memory operand
+ * layout (K-major core matrices), decoded once per (format, operand type) from the bitmaps and the
+ * bit-ordered values (tile.py:123-131): b_dtype 0 -> tf32 (cvt.rna, 256 B per block), 1 -> bf16,
+ * 2 -> fp16 (round to nearest, 128 B per block).  out_bytes >= rsh_tc_fragment_bytes(). */
+size_t rsh_tc_fragment_bytes(int64_t n_blocks, int32_t b_dtype);
+int rsh_tc_fragments(int64_t n_rows, int64_t n_entries, const uint64_t* bitmaps, const float* tc_values,
+                     int64_t n_blocks, int64_t n_res, int32_t b_dtype, const void* sched, size_t sched_bytes,
+                     void* out, size_t out_bytes, cudaStream_t stream);
+
 /* rsh_spmm_tc: the same contract with the window blocks on the tensor cores (tcgen05.mma,
- * fp32 accumulation in TMEM): b_dtype 0 -> TF32 operands, 1 -> BF16, 2 -> FP16.  N must be 128
- * or 256, B rows 16-byte aligned; residual / uncovered rows run on CUDA cores in the same launch.
- * l1: 1 gathers B rows through L1 (cp.async.ca), 0 through L2 only (cp.async.cg). */
+ * fp32 accumulation in TMEM): b_dtype 0 -> TF32 operands, 1 -> BF16, 2 -> FP16.  N in
+ * {32, 64, 128, 256} (fp32 B) or {64, 128, 256} (half B); B rows 16-byte aligned.  b_rows = rows
+ * of B (the TMA tensor map's extent: B rows are staged into shared memory by tile::gather4, and
+ * padding slots read as zeros); fragments = rsh_tc_fragments(..., b_dtype) of this format.
+ * Residual / uncovered rows run on CUDA cores in the same launch.  flags: bit 13 = "no window
+ * needs the fix-up kernels" (as rsh_spmm_cc's accum bit 14); bits 0/2 are perf probes (skip the
+ * gathers / the MMAs; results invalid). */
 int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const uint64_t* bitmaps,
-                const int32_t* col_id, const float* tc_values, int64_t n_blocks, const int32_t* res_row_id,
-                const int64_t* res_offset, const int32_t* res_col_id, const float* res_values, int64_t n_res,
-                const void* B, int64_t ldb, int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t l1,
-                void* sched, size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
+                const int32_t* col_id, const void* fragments, size_t fragment_bytes, int64_t n_blocks,
+                const int32_t* res_row_id, const int64_t* res_offset, const int32_t* res_col_id,
+                const float* res_values, int64_t n_res, const void* B, int64_t b_rows, int64_t ldb,
+                int32_t b_dtype, int64_t N, float* C, int64_t ldc, int32_t flags, void* sched,
+                size_t sched_bytes, void* partials, size_t partial_bytes, cudaStream_t stream);
 
 /* ---- format checks and decode: tile.py:176-267 validate_rstile, tile.py:270-307 decode_rstile.
  *      rsh_validate writes rsh_report_slots() int64 facts (first offending index per check,
@@ -192,10 +206,6 @@ int rsh_decode(int64_t n_rows, int64_t n_cols, const int32_t* row_window_id, con
                const int32_t* res_col_id, const float* res_values, int64_t res_nnz, int64_t* out_row_ptr,
                int32_t* out_col_idx, float* out_values, int64_t* dup_out, void* ws, size_t ws_bytes,
                cudaStream_t stream);
-
-/* debug: per-CTA role cycle counters of the last rsh_spmm_tc launches run with l1 bit 4 set
- * (host_out: 1024 x 16 uint64), cleared after reading */
-int rsh_tc_profile(unsigned long long* host_out);
 
 /* ---- verification: core.py:398-408 max_relative_error, result in out[0] (device double) - */
 int rsh_max_relative_error(const float* c, const float* ref, int64_t rows, int64_t n_features, int64_t ldc,

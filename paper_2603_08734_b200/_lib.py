@@ -55,9 +55,10 @@ SIGNATURES = {
     "rsh_schedule_rowmajor": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _sz, _vp]),
     "rsh_spmm_cc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
                                    _i32, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
-    "rsh_spmm_tc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
-                                   _i32, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
-    "rsh_tc_profile": (ctypes.c_int, [_vp]),
+    "rsh_tc_fragment_bytes": (_sz, [_i64, _i32]),
+    "rsh_tc_fragments": (ctypes.c_int, [_i64, _i64, _vp, _vp, _i64, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
+    "rsh_spmm_tc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _sz, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
+                                   _i64, _i32, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
     "rsh_report_slots": (ctypes.c_int, []),
     "rsh_validate_workspace": (_sz, [_i64, _i64, _i64]),
     "rsh_validate": (ctypes.c_int, [_i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64,

@@ -315,6 +315,7 @@ class SpmmPlan:
         self.groups, self.window_units, self.units, self.partial_slots, self.uncovered = h[:5]
         self.fixup_windows = h[6]
         self._ws = {}
+        self._frags = {}
         self.ulist = None
         if chunk == CHUNK_CC_LIST:
             # the streaming kernel's pre-decoded window list (8 bytes per tc nonzero)
@@ -324,6 +325,17 @@ class SpmmPlan:
             call("rsh_schedule_rowmajor", t.n_rows, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id), _ptr(t.values),
                  t.n_blocks, tc_nnz, t.n_res, _ptr(self.buf), self.nbytes, _ptr(self.ulist), 8 * self.ulist.numel(),
                  _stream(stream))
+
+    def fragments(self, t: DeviceTile, b_dtype: int, stream=None) -> torch.Tensor:
+        """The tensor-core kernel's schedule-time fragments for one operand type (rsh_tc_fragments),
+        built on first use."""
+        if b_dtype not in self._frags:
+            nbytes = lib().rsh_tc_fragment_bytes(t.n_blocks, b_dtype)
+            fr = torch.empty((nbytes + 15) // 16 * 16, dtype=torch.uint8, device=t.device)
+            call("rsh_tc_fragments", t.n_rows, t.n_entries, _ptr(t.bitmaps), _ptr(t.values), t.n_blocks, t.n_res,
+                 b_dtype, _ptr(self.buf), self.nbytes, _ptr(fr), fr.numel(), _stream(stream))
+            self._frags[b_dtype] = fr
+        return self._frags[b_dtype]
 
     def workspace(self, N: int, accum: int, dev, stream=None) -> torch.Tensor:
         """Zero-filled SpMM workspace (control block + chunk partials) for one stream."""
@@ -342,6 +354,8 @@ ROWMAJOR_LIST = os.environ.get("RSH_ROWMAJOR_LIST", "1") != "0"
 # rsh_spmm_cc tuning knobs (accum bits 1..): development override through RSH_CC_VARIANT
 CC_VARIANT = int(os.environ.get("RSH_CC_VARIANT", "0"))
 NO_FIXUP = 8192  # cc variant bit: the schedule has no window the fix-up kernels must reduce
+# rsh_spmm_tc perf-probe knobs (bits 0-2 skip gathers / decode / MMA: results invalid); development only
+TC_FLAGS = int(os.environ.get("RSH_TC_FLAGS", "0"))
 
 
 def spmm_plan(t: DeviceTile, chunk: int = CHUNK_CC) -> SpmmPlan:
@@ -357,11 +371,16 @@ def spmm_plan(t: DeviceTile, chunk: int = CHUNK_CC) -> SpmmPlan:
     return pl
 
 
+TC_N = {torch.float32: (32, 64, 128, 256), torch.bfloat16: (64, 128, 256), torch.float16: (64, 128, 256)}
+
+
 def tc_eligible(t: DeviceTile, b: torch.Tensor, accumulate: str = "f32") -> bool:
-    """The tensor-core kernel handles N in {128, 256} with f32 accumulation and 16-B aligned rows."""
+    """The tensor-core kernel handles N in {32, 64, 128, 256} (fp32 B; {64, 128, 256} for half B)
+    with f32 accumulation and 16-B aligned rows (csrc/spmm_tc.cu)."""
     n = int(b.shape[1])
     eb = b.element_size()
-    return (accumulate == "f32" and n in (128, 256) and b.data_ptr() % 16 == 0 and (b.stride(0) * eb) % 16 == 0)
+    return (accumulate == "f32" and n in TC_N.get(b.dtype, ()) and b.data_ptr() % 16 == 0
+            and (b.stride(0) * eb) % 16 == 0)
 
 
 def resolve_math(math: str, b: torch.Tensor, t: DeviceTile, accumulate: str) -> str:
@@ -375,12 +394,13 @@ def resolve_math(math: str, b: torch.Tensor, t: DeviceTile, accumulate: str) -> 
     if math in ("auto", "fp32") or accumulate != "f32":
         return "cc"
     if not tc_eligible(t, b, accumulate):
-        raise ValueError(f"math={math!r} needs N in {{128, 256}}, f32 accumulation and 16-byte aligned B rows")
+        raise ValueError(f"math={math!r} needs N in {TC_N.get(b.dtype, ())} for {b.dtype}, f32 accumulation and "
+                         "16-byte aligned B rows")
     return "tc"
 
 
 def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None, accumulate: str = "f32",
-                stream=None, math: str = "auto", l1: bool = True, cc_variant: int | None = None) -> torch.Tensor:
+                stream=None, math: str = "auto", cc_variant: int | None = None) -> torch.Tensor:
     """C = A @ B with A an RS-Tile on device; B [n_cols, N] f32/bf16/f16 row-major on device.
     Returns (or fills) C [n_rows, N] float32.  accumulate: "f32" | "f64" (execute.py:33-49);
     math: "auto" / "fp32" (CUDA-core FMA) | "tf32" / "tc" (tensor cores, see resolve_math)."""
@@ -411,13 +431,21 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
         chunk = CHUNK_CC
     plan = spmm_plan(t, chunk)
     part = plan.workspace(N, acc, b.device, stream)
-    flags = int(l1) if path == "tc" else acc | (cc_variant << 1)
-    if plan.fixup_windows == 0:
-        flags |= NO_FIXUP << 1 if path != "tc" else NO_FIXUP
-    call("rsh_spmm_tc" if path == "tc" else "rsh_spmm_cc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id),
-         _ptr(t.values), t.n_blocks, _ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id),
-         _ptr(t.res_values), t.n_res, _ptr(b), b.stride(0), _BDT[b.dtype], N, _ptr(out), out.stride(0),
-         flags, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
+    res = (_ptr(t.res_row_id), _ptr(t.res_offset), _ptr(t.res_col_id), _ptr(t.res_values), t.n_res)
+    if path == "tc":
+        flags = (NO_FIXUP if plan.fixup_windows == 0 else 0) | TC_FLAGS
+        fr = plan.fragments(t, _BDT[b.dtype], stream)
+        call("rsh_spmm_tc", t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id), _ptr(fr),
+             fr.numel(), t.n_blocks, *res, _ptr(b), int(b.shape[0]), b.stride(0), _BDT[b.dtype], N, _ptr(out),
+             out.stride(0), flags, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
+    else:
+        fmt = (t.n_rows, t.window_size, t.n_entries, _ptr(t.bitmaps), _ptr(t.col_id), _ptr(t.values), t.n_blocks,
+               *res)
+        flags = acc | (cc_variant << 1)
+        if plan.fixup_windows == 0:
+            flags |= NO_FIXUP << 1
+        call("rsh_spmm_cc", *fmt, _ptr(b), b.stride(0), _BDT[b.dtype], N, _ptr(out), out.stride(0),
+             flags, _ptr(plan.buf), plan.nbytes, _ptr(part), part.numel(), _stream(stream))
     return out
 
 

@@ -102,7 +102,7 @@ def hybrid_spmm(m, b, cfg: ExecConfig | None = None, out=None):
         if ids.size and (int(ids.min()) < 0 or int(ids.max()) >= bd.shape[0]):
             raise FormatError("col_id references a column outside B's row range")
     t = tile_to_device(m)
-    bt = torch.from_numpy(np.ascontiguousarray(bd, np.float32)).to(t.device)
+    bt = torch.from_numpy(np.array(bd, np.float32, order="C", copy=True)).to(t.device)
     c = _device_spmm(t, bt, cfg)
     if cfg.check_against_oracle:
         _verify(t, bt, c)

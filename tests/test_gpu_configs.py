@@ -86,7 +86,7 @@ def test_format_bit_exact_with_oracle(config):
 
 
 def test_products_against_fp64_oracle(config):
-    from paper_2603_08734_b200.device import spmm_device
+    from paper_2603_08734_b200.device import spmm_device, tc_eligible
     name, w, a, b, t = config
     bt = torch.from_numpy(b).cuda()
     if w.dtype == "bf16":
@@ -94,7 +94,7 @@ def test_products_against_fp64_oracle(config):
     c_fp32 = spmm_device(t, bt, math="fp32")
     c_fp32_again = spmm_device(t, bt, math="fp32")
     assert torch.equal(c_fp32, c_fp32_again)
-    use_tc = w.n_features in (128, 256)
+    use_tc = tc_eligible(t, bt)
     c_tc = spmm_device(t, bt, math="tc") if use_tc else None
     if c_tc is not None:
         assert torch.equal(c_tc, spmm_device(t, bt, math="tc"))

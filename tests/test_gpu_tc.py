@@ -32,7 +32,7 @@ def _b(n, d, seed, dtype=torch.float32):
     return torch.from_numpy(x).cuda().to(dtype)
 
 
-@pytest.mark.parametrize("d", [128, 256])
+@pytest.mark.parametrize("d", [32, 64, 128, 256])
 def test_tf32_matches_fp64_oracle(small_corpus, d):
     from paper_2603_08734_b200.device import spmm_device
     for a in small_corpus:
@@ -49,7 +49,7 @@ def test_tf32_matches_fp64_oracle(small_corpus, d):
 
 
 @pytest.mark.parametrize("dt", ["bfloat16", "float16"])
-@pytest.mark.parametrize("d", [128, 256])
+@pytest.mark.parametrize("d", [64, 128, 256])
 def test_half_operands_on_tensor_cores(dt, d):
     from paper_2603_08734_b200 import synth
     from oracle import corpus  # noqa: E402
@@ -84,18 +84,18 @@ def test_tf32_rounding_is_not_truncation():
     assert O.rel_frobenius(c, ref64) <= 1e-6
 
 
-@pytest.mark.parametrize("l1", [True, False])
-def test_tc_split_invariance_and_determinism(l1):
+@pytest.mark.parametrize("d", [64, 128])
+def test_tc_split_invariance_and_determinism(d):
     from paper_2603_08734_b200 import synth
     from oracle import corpus  # noqa: E402
     from paper_2603_08734_b200.device import spmm_device
     a = corpus.generate_power_law(128, 4096, 40000, 2.0, seed=11)
-    b = _b(4096, 128, 11)
+    b = _b(4096, d, 11)
     outs = set()
     for k in (1, 4, 64, None):
         t = _tile(a, max_blocks_per_item=k)
         for _ in range(2):
-            outs.add(spmm_device(t, b, math="tf32", l1=l1).cpu().numpy().tobytes())
+            outs.add(spmm_device(t, b, math="tf32").cpu().numpy().tobytes())
     assert len(outs) == 1
 
 

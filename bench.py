@@ -35,9 +35,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SpMM GFLOP/s (2*nnz*N/t)"
 # profiles/r02_gather_plateau.txt: random 512-B B rows gathered with LDG.128 by 148 SMs at full
-# occupancy (the plateau of every path measured: LDG, cp.async, cp.async.bulk, TMA gather4)
-GATHER_ROOF_L2_GBS = 19673.0   # 64 MB footprint (L2-resident)
-GATHER_ROOF_HBM_GBS = 7462.0   # 2 GB footprint (from HBM)
+# occupancy -- the plateau of every path measured (LDG, cp.async, cp.async.bulk, TMA gather4)
+GATHER_ROOF_L2_GBS = 19648.0   # 64 MB footprint (L2-resident)
+GATHER_ROOF_HBM_GBS = 7289.0   # 2 GB footprint (from HBM)
 
 
 def _peaks() -> dict:

@@ -109,6 +109,13 @@ int rsh_knn(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, cons
             const int32_t* at_col_idx, const double* w, const double* wsum, int32_t k, int32_t max_candidates,
             int64_t hub_cap, int32_t* nbr, double* nsim, int32_t* ncount, unsigned long long* stats,
             cudaStream_t stream);
+/* reorder.py:168-194 build_candidates: rows sharing a column with each row (itself excluded), the
+ * max_candidates (<= 1024) with the most shared columns when more (ties to the lower row), ascending:
+ * cand[r * max_candidates .. + cand_cnt[r]]; stats[0] = rows whose candidate set overflowed the
+ * per-row device table (their lists are truncated). */
+int rsh_candidates(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, const int64_t* at_row_ptr,
+                   const int32_t* at_col_idx, int32_t max_candidates, int64_t hub_cap, int32_t* cand,
+                   int32_t* cand_cnt, unsigned long long* stats, cudaStream_t stream);
 int rsh_pair_dis(const int64_t* row_ptr, const int32_t* col_idx, const double* w, const double* wsum,
                  const int64_t* order, int64_t m, double* dis, cudaStream_t stream);
 int rsh_two_opt_sweep(const int64_t* row_ptr, const int32_t* col_idx, const double* w, const double* wsum,
@@ -210,6 +217,14 @@ int rsh_decode(int64_t n_rows, int64_t n_cols, const int32_t* row_window_id, con
 /* ---- verification: core.py:398-408 max_relative_error, result in out[0] (device double) - */
 int rsh_max_relative_error(const float* c, const float* ref, int64_t rows, int64_t n_features, int64_t ldc,
                            double* out, cudaStream_t stream);
+/* core.py:380-395 oracle_spmm from the CSR: f64 accumulation per row in CSR order, f32 store */
+int rsh_csr_spmm_f64(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
+                     const float* B, int64_t ldb, int64_t N, float* C, int64_t ldc, cudaStream_t stream);
+
+/* ---- structure metrics: metrics.py:28-63 tile_density.  out (device uint64[2]) = [row windows
+ *      (consecutive equal row_window_id), occupied rows of those windows]. ------------------- */
+int rsh_tile_density(const int32_t* row_window_id, const int64_t* row_window_offset, int64_t n_entries,
+                     const uint64_t* bitmaps, unsigned long long* out, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

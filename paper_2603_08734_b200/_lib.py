@@ -59,6 +59,9 @@ SIGNATURES = {
     "rsh_tc_fragments": (ctypes.c_int, [_i64, _i64, _vp, _vp, _i64, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
     "rsh_spmm_tc": (ctypes.c_int, [_i64, _i32, _i64, _vp, _vp, _vp, _sz, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64,
                                    _i64, _i32, _i64, _vp, _i64, _i32, _vp, _sz, _vp, _sz, _vp]),
+    "rsh_candidates": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
+    "rsh_csr_spmm_f64": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "rsh_tile_density": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
     "rsh_report_slots": (ctypes.c_int, []),
     "rsh_validate_workspace": (_sz, [_i64, _i64, _i64]),
     "rsh_validate": (ctypes.c_int, [_i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64,

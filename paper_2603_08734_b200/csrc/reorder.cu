@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn(const int64_t* __restric
                                                        const int32_t* __restrict__ tci, const double* __restrict__ w,
                                                        const double* __restrict__ wsum, int k, int max_cand,
                                                        int64_t hub_cap, int32_t* nbr, double* nsim, int32_t* ncount,
-                                                       unsigned long long* stats) {
+                                                       unsigned long long* stats, int32_t* cand, int32_t* cand_cnt) {
   extern __shared__ __align__(16) unsigned char knn_smem[];
   KnnSmem& sm = reinterpret_cast<KnnSmem*>(knn_smem)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -186,8 +186,36 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn(const int64_t* __restric
         }
       }
     }
-    // exact similarities of the kept candidates
     const int n_cand = n_occ < max_cand ? n_occ : max_cand;
+    if (cand) {
+      // build_candidates (reorder.py:168-194): the kept rows in ascending order
+      int P = 32;
+      while (P < n_cand) P <<= 1;
+      for (int i = lane; i < P; i += 32)
+        sm.sk[i] = i < n_cand ? ((sm.sk[i] >> 10) & 0x7FFFFFFFull) : ~0ull;
+      __syncwarp();
+      for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int i = lane; i < P; i += 32) {
+            const int j = i ^ stride;
+            if (j > i) {
+              const bool up = (i & size) == 0;
+              const unsigned long long x = sm.sk[i], y = sm.sk[j];
+              if ((x > y) == up) {
+                sm.sk[i] = y;
+                sm.sk[j] = x;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      for (int i = lane; i < n_cand; i += 32) cand[r * (int64_t)max_cand + i] = (int32_t)sm.sk[i];
+      if (lane == 0) cand_cnt[r] = n_cand;
+      __syncwarp();
+      continue;
+    }
+    // exact similarities of the kept candidates
     for (int i = lane; i < n_cand; i += 32) {
       const int64_t u = (int64_t)((sm.sk[i] >> 10) & 0x7FFFFFFFull);
       sm.sim[i] = row_sim(rp, ci, w, wsum, r, u);
@@ -338,12 +366,35 @@ int rsh_knn(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, cons
   const int64_t cap = 16LL * sm_count();
   if (blocks > cap) blocks = cap;
   k_knn<<<(unsigned)blocks, 32 * kKnnWarps, smem, st>>>(row_ptr, col_idx, n_rows, at_row_ptr, at_col_idx, w, wsum, k,
-                                                       max_candidates, hub_cap, nbr, nsim, ncount, stats);
+                                                       max_candidates, hub_cap, nbr, nsim, ncount, stats, nullptr, nullptr);
   RSH_LAUNCHED("k_knn");
   return kOk;
 }
 
 // 1 - sim over the m-1 adjacent pairs of a device order (the objective's terms)
+// reorder.py:168-194 build_candidates: per row r, the rows sharing a column with r (r excluded),
+// the max_candidates with the largest shared-column count when more (ties to the lower row), in
+// ascending order: cand[r * max_candidates .. + cand_cnt[r]].  stats[0] += rows whose candidate set
+// overflowed the per-row table (then truncated: the caller treats that as an error).
+int rsh_candidates(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, const int64_t* at_row_ptr,
+                   const int32_t* at_col_idx, int32_t max_candidates, int64_t hub_cap, int32_t* cand,
+                   int32_t* cand_cnt, unsigned long long* stats, cudaStream_t st) {
+  if (max_candidates < 1) return fail(kInvalid, "max_candidates must be at least 1");
+  if (max_candidates > kKnnCap) return fail(kInvalid, "max_candidates above the device table (%d)", kKnnCap);
+  RSH_CUDA(cudaMemsetAsync(stats, 0, sizeof(unsigned long long), st));
+  if (!n_rows) return kOk;
+  const size_t smem = sizeof(KnnSmem) * kKnnWarps;
+  RSH_CUDA(cudaFuncSetAttribute(k_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t blocks = (n_rows + kKnnWarps - 1) / kKnnWarps;
+  const int64_t cap = 16LL * sm_count();
+  if (blocks > cap) blocks = cap;
+  k_knn<<<(unsigned)blocks, 32 * kKnnWarps, smem, st>>>(row_ptr, col_idx, n_rows, at_row_ptr, at_col_idx, nullptr, nullptr,
+                                                       1, max_candidates, hub_cap, nullptr, nullptr, nullptr, stats,
+                                                       cand, cand_cnt);
+  RSH_LAUNCHED("k_knn(candidates)");
+  return kOk;
+}
+
 int rsh_pair_dis(const int64_t* row_ptr, const int32_t* col_idx, const double* w, const double* wsum,
                  const int64_t* order, int64_t m, double* dis, cudaStream_t st) {
   if (m > 1) {

@@ -384,3 +384,71 @@ int rsh_decode(int64_t n_rows, int64_t n_cols, const int32_t* row_window_id, con
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// core.py:380-395 oracle_spmm: C = A @ B from the CSR, every row accumulated in f64 in CSR order
+// (values and B widened to f64 exactly, as the reference's astype(np.float64)), stored as f32;
+// rows without nonzeros are zero.  Warp per row, lanes across features.
+// ---------------------------------------------------------------------------------------------
+namespace rsh {
+__global__ void k_csr_spmm_f64(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               const float* __restrict__ v, int64_t n_rows, const float* __restrict__ B, int64_t ldb,
+                               int64_t N, float* __restrict__ C, int64_t ldc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w0; r < n_rows; r += nw) {
+    const int64_t s = rp[r], e = rp[r + 1];
+    for (int64_t f = lane; f < N; f += 32) {
+      double acc = 0.0;
+      for (int64_t p = s; p < e; ++p) acc += (double)__ldg(v + p) * (double)__ldg(B + (int64_t)__ldg(ci + p) * ldb + f);
+      C[r * ldc + f] = (float)acc;
+    }
+  }
+}
+
+// metrics.py:28-63 tile_density: one thread per row-window head (consecutive equal row_window_id
+// are one window, tile.py segments); the OR of the window's blocks' row bytes gives its occupied
+// rows.  out[0] += windows, out[1] += occupied window rows.
+__global__ void k_tile_density(const int32_t* __restrict__ rwid, const int64_t* __restrict__ off, int64_t E,
+                               const unsigned long long* __restrict__ bm, unsigned long long* out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  if (e > 0 && rwid[e] == rwid[e - 1]) return;
+  int64_t e2 = e + 1;
+  while (e2 < E && rwid[e2] == rwid[e]) ++e2;
+  unsigned long long acc = 0;
+  for (int64_t b = off[e]; b < off[e2]; ++b) acc |= bm[b];
+  uint32_t rows = 0;
+  for (int i = 0; i < 8; ++i) rows += ((acc >> (8 * i)) & 0xffull) != 0;
+  atomicAdd(out, 1ull);
+  atomicAdd(out + 1, (unsigned long long)rows);
+}
+}  // namespace rsh
+
+extern "C" {
+
+int rsh_csr_spmm_f64(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
+                     const float* B, int64_t ldb, int64_t N, float* C, int64_t ldc, cudaStream_t st) {
+  if (n_rows < 0 || N < 0 || ldb < N || ldc < N) return rsh::fail(rsh::kInvalid, "rsh_csr_spmm_f64: bad shape");
+  if (n_rows == 0 || N == 0) return rsh::kOk;
+  int64_t blocks = (n_rows + 7) / 8;
+  const int64_t cap = 32LL * rsh::sm_count();
+  if (blocks > cap) blocks = cap;
+  rsh::k_csr_spmm_f64<<<(unsigned)blocks, 256, 0, st>>>(row_ptr, col_idx, values, n_rows, B, ldb, N, C, ldc);
+  RSH_LAUNCHED("k_csr_spmm_f64");
+  return rsh::kOk;
+}
+
+// out (device uint64[2]) = [windows, occupied window rows]
+int rsh_tile_density(const int32_t* row_window_id, const int64_t* row_window_offset, int64_t n_entries,
+                     const uint64_t* bitmaps, unsigned long long* out, cudaStream_t st) {
+  RSH_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st));
+  if (n_entries <= 0) return rsh::kOk;
+  rsh::k_tile_density<<<rsh::grid_1d(n_entries), rsh::kThreads, 0, st>>>(
+      row_window_id, row_window_offset, n_entries, (const unsigned long long*)bitmaps, out);
+  RSH_LAUNCHED("k_tile_density");
+  return rsh::kOk;
+}
+
+}  // extern "C"

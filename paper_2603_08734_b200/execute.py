@@ -117,6 +117,33 @@ __all__ = ["ExecConfig", "VerificationError", "hybrid_spmm", "ORACLE_TOLERANCE"]
 # one-window or residual-only sub-format, so the arithmetic is the product kernel's
 # ---------------------------------------------------------------------------------------------
 
+def oracle_spmm(a, b) -> DenseMatrix:
+    """core.py:380-395 on device: C = A @ B with every row accumulated in f64 in CSR order (A's
+    values and B widened exactly), stored as f32; empty rows are zero.  ``a`` is a CsrMatrix (or
+    a DeviceCsr), ``b`` a DenseMatrix (or a CUDA tensor; a CUDA tensor is returned)."""
+    import torch
+
+    from ._lib import call
+    from .device import DeviceCsr, _ptr, _stream, require_cuda
+    host = not isinstance(a, DeviceCsr)
+    n_b = b.n_rows if isinstance(b, DenseMatrix) else int(b.shape[0])
+    if a.n_cols != n_b:
+        raise ValueError(f"dimension mismatch: A is {a.n_rows}x{a.n_cols}, B has {n_b} rows")
+    dev = require_cuda()
+    d = DeviceCsr.from_host(a, dev) if host else a
+    if isinstance(b, DenseMatrix):
+        bt = torch.from_numpy(np.array(b.data, np.float32, order="C", copy=True)).to(d.device)
+    else:
+        bt = b.float().contiguous()
+    n_feat = int(bt.shape[1])
+    c = torch.empty((d.n_rows, n_feat), dtype=torch.float32, device=d.device)
+    call("rsh_csr_spmm_f64", _ptr(d.row_ptr), _ptr(d.col_idx), _ptr(d.values), d.n_rows, _ptr(bt), bt.stride(0),
+         n_feat, _ptr(c), c.stride(0), _stream())
+    if not isinstance(b, DenseMatrix):
+        return c
+    return DenseMatrix(d.n_rows, n_feat, c.cpu().numpy())
+
+
 @dataclass(frozen=True)
 class Fragment8x8:
     """execute.py:52-62: dense row-major 8x8 expansion of one bitmap block."""

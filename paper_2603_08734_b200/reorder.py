@@ -189,6 +189,36 @@ def knn_device(ctx: "_Ctx", k: int = 8, max_candidates: int = 256, hub_cap: int 
     return nbr[:n], sim[:n], cnt[:n], int(stats.item())
 
 
+def build_candidates(a: CsrMatrix, max_candidates: int = 256, hub_cap: int | None = None) -> list:
+    """reorder.py:168-194 on device (rsh_candidates): for every row, the rows sharing at least one
+    column with it (never itself), the max_candidates with the largest shared-column count when
+    there are more (ties to the lower row index), ascending, as int64 arrays.  Raises ValueError
+    when a row's candidate set overflows the device's per-row table (pass ``hub_cap`` to skip
+    columns of higher degree, as build_knn does)."""
+    import torch
+    from ._lib import call
+    from .device import _ptr, _stream
+    from .gnn import transpose_device
+    if max_candidates < 1:
+        raise ValueError("max_candidates must be at least 1")
+    ctx = _Ctx(a, 0.5)
+    d = ctx.d
+    n = d.n_rows
+    if n == 0:
+        return []
+    at = transpose_device(d)
+    cand = torch.zeros((n, max_candidates), dtype=torch.int32, device=d.device)
+    cnt = torch.zeros(n, dtype=torch.int32, device=d.device)
+    stats = torch.zeros(1, dtype=torch.int64, device=d.device)
+    call("rsh_candidates", _ptr(d.row_ptr), _ptr(d.col_idx), n, _ptr(at.row_ptr), _ptr(at.col_idx), max_candidates,
+         (1 << 62) if hub_cap is None else int(hub_cap), _ptr(cand), _ptr(cnt), _ptr(stats), _stream())
+    if int(stats.item()):
+        raise ValueError(f"{int(stats.item())} rows have more distinct candidate rows than the device table holds; "
+                         "pass hub_cap to bound the columns walked")
+    cn, cd = cnt.cpu().numpy(), cand.cpu().numpy()
+    return [cd[r, :cn[r]].astype(np.int64) for r in range(n)]
+
+
 def build_knn(a: CsrMatrix, w: ColumnWeights | None = None, candidates=None, k: int = 8,
               max_candidates: int = 256, hub_cap: int | None = None) -> KnnGraph:
     """reorder.py:158-230 (build_candidates + build_knn) on device.  ``candidates`` is accepted

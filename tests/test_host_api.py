@@ -125,8 +125,32 @@ def test_max_relative_error_matches_reference_definition():
 @pytest.mark.skipif(gpu_available(), reason="checks the no-GPU behaviour")
 def test_compute_fails_loudly_without_gpu():
     a = P.CsrMatrix.from_dense(np.eye(4, dtype=np.float32))
-    with pytest.raises(RuntimeError, match="CUDA"):
-        P.partition_rows(a)
+    b = P.DenseMatrix.from_array(np.ones((4, 2), np.float32))
+    for fn in (lambda: P.partition_rows(a), lambda: P.oracle_spmm(a, b), lambda: P.build_candidates(a),
+               lambda: P.threshold_sweep(a, [2])):
+        with pytest.raises(RuntimeError, match="CUDA"):
+            fn()
+
+
+# names of the reference's public API (rstile __init__.py __all__) on the path SURVEY 8 scopes:
+# the hot path (a1-a21), its drop-in types and the 8(f) rows; out of scope by SURVEY 2: CooMatrix,
+# RowStats/row_stats, generate_power_law, Matrix Market / DMAT I/O, reorder_gain/ReorderGain
+REFERENCE_NAMES = [
+    "CsrMatrix", "DenseMatrix", "ExecConfig", "FormatError", "Fragment8x8", "KnnGraph", "PartitionParams",
+    "PartitionPlan", "Permutation", "ReorderParams", "ResidualPart", "RsTileMatrix", "StorageReport", "TcPart",
+    "TileDensityReport", "VerificationError", "build_candidates", "build_knn", "build_rstile", "column_weights",
+    "csr_equal", "decode_rstile", "decode_tile", "estimate_thresholds", "exec_residual", "exec_tc_window",
+    "hybrid_spmm", "isolation_adjust", "load_permutation", "load_rstile", "max_relative_error", "mst_order",
+    "oracle_spmm", "partition_rows", "permutation_objective", "permute_rows", "refine_2opt", "reorder_pipeline",
+    "save_permutation", "save_rstile", "split_long_work", "storage_report", "sweep_csv", "threshold_sweep",
+    "tile_density", "validate_plan", "validate_rstile", "w_jaccard",
+]
+
+
+def test_public_api_keeps_reference_names():
+    for name in REFERENCE_NAMES:
+        assert hasattr(P, name), name
+        assert name in P.__all__, name
 
 
 def test_synthetic_config_counts_match_survey():

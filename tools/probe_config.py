@@ -55,20 +55,20 @@ def main():
     out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(3):
-        spmm_device(t, bt, out=out, math=args.math, l1=args.l1, cc_variant=args.ccv)
+        spmm_device(t, bt, out=out, math=args.math, cc_variant=args.ccv)
     torch.cuda.synchronize()
     times = []
     for _ in range(args.iters):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        spmm_device(t, bt, out=out, math=args.math, l1=args.l1, cc_variant=args.ccv)
+        spmm_device(t, bt, out=out, math=args.math, cc_variant=args.ccv)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     ms = float(np.median(times))
     flops = 2.0 * a.nnz * b.shape[1]
-    print(f"spmm[{args.math}, l1={args.l1}] median {ms:.3f} ms  min {min(times):.3f}  -> {flops / ms / 1e6:.1f} GFLOP/s", flush=True)
+    print(f"spmm[{args.math}] median {ms:.3f} ms  min {min(times):.3f}  -> {flops / ms / 1e6:.1f} GFLOP/s", flush=True)
     if args.check:
         import oracle as O
         c = out.cpu().numpy()

@@ -66,6 +66,10 @@ int rsh_plan_windows(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_r
 
 /* ---- RS-Tile build: tile.py:102-144 build_rstile (TC part).  With chunk == NULL the
  *      entry arrays are not written (the caller supplies explicit segments). -------------- */
+/* TcPart.values size (tile.py:123-131): sum over windows of their rows' nonzeros; win_count NULL
+ * means min(window_size, n_rows - start).  out: device int64[1]. */
+int rsh_window_nnz(const int64_t* row_ptr, int64_t n_rows, const int32_t* win_start, const int32_t* win_count,
+                   int64_t n_win, int32_t window_size, long long* out, cudaStream_t stream);
 size_t rsh_fill_workspace(int64_t nnz, int64_t n_blocks);
 int rsh_build_fill(const int64_t* row_ptr, const int32_t* col_idx, const float* values, int64_t n_rows,
                    int64_t nnz, int32_t window_size, const int32_t* win_start, const int32_t* win_count,

@@ -62,6 +62,7 @@ SIGNATURES = {
     "rsh_candidates": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "rsh_csr_spmm_f64": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _vp]),
     "rsh_tile_density": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
+    "rsh_window_nnz": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp]),
     "rsh_report_slots": (ctypes.c_int, []),
     "rsh_validate_workspace": (_sz, [_i64, _i64, _i64]),
     "rsh_validate": (ctypes.c_int, [_i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64,

@@ -426,6 +426,22 @@ __global__ void k_transpose_gather(const int32_t* __restrict__ perm, const int32
 
 }  // namespace rsh
 
+namespace rsh {
+__global__ void k_window_nnz(const int64_t* __restrict__ rp, int64_t n_rows, const int32_t* __restrict__ ws,
+                             const int32_t* __restrict__ wc, int64_t n_win, int32_t window_size,
+                             unsigned long long* out) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (w < n_win) {
+    const int64_t s = ws[w];
+    int64_t c = wc ? (int64_t)wc[w] : (n_rows - s < window_size ? n_rows - s : window_size);
+    v = (unsigned long long)(rp[s + c] - rp[s]);
+  }
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+}  // namespace rsh
+
 extern "C" {
 
 size_t rsh_partition_workspace(int64_t n_rows) {
@@ -749,6 +765,19 @@ int rsh_transpose_csr(const int64_t* row_ptr, const int32_t* col_idx, const floa
   }
   size_t t = cb;
   RSH_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t, cnt, out_row_ptr, (int)(n_cols + 1), st));
+  return kOk;
+}
+
+// Nonzeros the window part of the format holds (the size of TcPart.values, tile.py:123-131):
+// sum over windows of row_ptr[start + count] - row_ptr[start]; count NULL means
+// min(window_size, n_rows - start).  out: device int64[1].
+int rsh_window_nnz(const int64_t* row_ptr, int64_t n_rows, const int32_t* win_start, const int32_t* win_count,
+                   int64_t n_win, int32_t window_size, long long* out, cudaStream_t st) {
+  RSH_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), st));
+  if (n_win <= 0) return kOk;
+  k_window_nnz<<<grid_1d(n_win), kThreads, 0, st>>>(row_ptr, n_rows, win_start, win_count, n_win, window_size,
+                                                     (unsigned long long*)out);
+  RSH_LAUNCHED("k_window_nnz");
   return kOk;
 }
 

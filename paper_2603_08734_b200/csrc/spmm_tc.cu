@@ -349,6 +349,9 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
     // ------------------------------------------------------------------ MMA issuers
     const int p = warp - kMma0;
     int64_t q = 0;
+    const bool no_mma = a.flags & 4;  // perf-probe knob (results invalid)
+    const uint64_t adesc0 = umma_desc(smem_u32(sA), G::LBO, G::SBO, G::layout);
+    const uint64_t bdesc0 = umma_desc(smem_u32(sF), 128, 256, 0);
     for (int64_t ub = p; u0 + ub < u1; ub += 32 * P) {
       // the block ranges of this pipeline's next 32 units, one per lane
       const int64_t ul = ub + (int64_t)P * lane;
@@ -374,16 +377,19 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
                 const int ss = p * SSP + (int)(q % SSP);
                 mbar_wait(full + ss, (uint32_t)((q / SSP) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                // descriptors: the 14-bit start-address field (bytes >> 4) of the stage-0 descriptors
+                // plus the stage / step / tile offset (shared memory < 256 KB: no carry out)
+                const uint64_t abase = adesc0 + (uint64_t)(((uint32_t)ss * (L::STEPS * G::ABYTES)) >> 4);
+                const uint64_t bbase = bdesc0 + (uint64_t)(((uint32_t)ss * (R * G::FB)) >> 4);
+                const uint32_t dbase = tmem + (uint32_t)(slot * G::MT * 8);
                 for (int st = 0; st < nsteps; ++st) {
-                  const uint64_t bdesc =
-                      umma_desc(smem_u32(sF + ((size_t)ss * R + st * G::BPS) * G::FB), 128, 256, 0);
+                  const uint64_t bdesc = bbase + (uint64_t)(((uint32_t)st * (G::BPS * G::FB)) >> 4);
+                  const uint32_t acc = first ? 0u : 1u;
 #pragma unroll
                   for (int t = 0; t < G::MT; ++t) {
-                    const uint64_t adesc = umma_desc(smem_u32(sA + ((size_t)ss * L::STEPS + st) * G::ABYTES + t * G::TILE),
-                                                     G::LBO, G::SBO, G::layout);
-                    const uint32_t d = tmem + (uint32_t)((slot * G::MT + t) * 8);
-                    const uint32_t acc = first ? 0u : 1u;
-                    if (a.flags & 4) continue;  // perf-probe knob: no MMA
+                    const uint64_t adesc = abase + (uint64_t)(((uint32_t)st * G::ABYTES + t * G::TILE) >> 4);
+                    const uint32_t d = dbase + (uint32_t)(t * 8);
+                    if (no_mma) continue;
                     if constexpr (G::EB == 4)
                       asm volatile("{\n.reg .pred pp;\nsetp.ne.b32 pp, %4, 0;\n"
                                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, pp;\n}" ::"r"(d),

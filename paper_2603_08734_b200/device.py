@@ -215,12 +215,10 @@ def fill_tile(a: DeviceCsr, plan: WindowPlan, resid: torch.Tensor, window_size: 
         ne = int(rwid.numel())
     bitmaps = torch.empty(max(nb, 1), dtype=torch.int64, device=dev)
     col_id = torch.empty(max(8 * nb, 1), dtype=torch.int32, device=dev)
-    if nw:
-        ws_l = plan.win_start.long()
-        cnt = plan.win_count.long() if plan.win_count is not None else torch.clamp(a.n_rows - ws_l, max=window_size)
-        tc_nnz = int((a.row_ptr[ws_l + cnt] - a.row_ptr[ws_l]).sum())
-    else:
-        tc_nnz = 0
+    wn = torch.zeros(1, dtype=torch.int64, device=dev)
+    call("rsh_window_nnz", _ptr(a.row_ptr), a.n_rows, _ptr(plan.win_start), _ptr(plan.win_count), nw, window_size,
+         _ptr(wn), st)
+    tc_nnz = int(wn.item())
     values = torch.empty(max(tc_nnz, 1), dtype=torch.float32, device=dev)
     nbytes = lib().rsh_fill_workspace(a.nnz, nb)
     ws = _ws(nbytes, dev)

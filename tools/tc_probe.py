@@ -40,12 +40,12 @@ def main():
         b = synth.workload_b(name, a.n_cols)
         tile = build_device(DeviceCsr.from_host(a, dev))
         bt = torch.from_numpy(b).to(dev)
-        if w.dtype == "bf16":
+        if w.dtype == "bf16" or os.environ.get("TC_BF16"):
             bt = bt.to(torch.bfloat16)
         print(f"{name}: nnz {a.nnz} blocks {tile.n_blocks} N {w.n_features} ({time.time() - t0:.1f} s)", flush=True)
         out_cc = torch.empty((a.n_rows, w.n_features), dtype=torch.float32, device=dev)
         out_tc = torch.empty_like(out_cc)
-        ms_cc = timeit(lambda: spmm_device(tile, bt, out=out_cc, math="fp32" if w.dtype == "f32" else "auto"))
+        ms_cc = timeit(lambda: spmm_device(tile, bt, out=out_cc, math="fp32" if bt.dtype == torch.float32 else "auto"))
         ms_tc = timeit(lambda: spmm_device(tile, bt, out=out_tc, math="tc"))
         d = (out_tc - out_cc).double()
         rel = float(d.norm() / out_cc.double().norm())

@@ -319,7 +319,7 @@ def _launches() -> int:
     return int(_lib.lib().rsh_launch_count())
 
 
-def ncu_traffic(args, kernel_regex: str, timeout_s: float = 240.0):
+def ncu_traffic(args, kernel_regex: str, math: str | None = None, timeout_s: float = 240.0):
     """dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the timed kernel, measured
     in this run: ncu over a child process that replays this workload (``--kernel-only``).  Also
     returns the L2 hit rate.  None when ncu is unavailable or fails (the line then says so)."""
@@ -330,7 +330,7 @@ def ncu_traffic(args, kernel_regex: str, timeout_s: float = 240.0):
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,"
            "gpu__time_duration.sum", "--clock-control", "none", "-k", f"regex:{kernel_regex}", "--launch-skip", "3",
            "--launch-count", "1", "--csv", sys.executable, os.path.abspath(__file__), "--kernel-only",
-           "--workload", args.workload, "--math", args.math]
+           "--workload", args.workload, "--math", math or args.math]
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, cwd=ROOT)
     except (OSError, subprocess.TimeoutExpired):
@@ -497,7 +497,8 @@ def run_single(args):
     e2e_value = flops / (float(np.mean(e2e_ms)) * 1e-3) / 1e9 if e2e_ms else None
 
     cpu = None if args.no_cpu_baseline else cpu_reference_sample(a, b_np.astype(np.float32), args.workload)
-    traffic = ncu_traffic(args, "k_spmm_stream|k_spmm_tc|k_spmm_cc")
+    # the same path the timed region ran (math = the fastest candidate)
+    traffic = ncu_traffic(args, "k_spmm_stream|k_spmm_tc|k_spmm_cc", math)
 
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,

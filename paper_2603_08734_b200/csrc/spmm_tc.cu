@@ -74,6 +74,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (n == (1u << 28)) __trap();
 }
 
+#ifdef RSH_TC_PROFILE
+// development build only: per-warp cycle counters [warp slot][0 total, 1 wait empty, 2 wait full,
+// 3 wait tempty, 4 wait tfull, 5 super-stages / units]
+__device__ unsigned long long g_tc_prof[148 * 40][8];
+#define PROF_WAIT(slot, stmt)                                      \
+  do {                                                             \
+    const long long _t = clock64();                                \
+    stmt;                                                          \
+    prof[slot] += clock64() - _t;                                  \
+  } while (0)
+#else
+#define PROF_WAIT(slot, stmt) stmt
+#endif
+
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
@@ -146,7 +160,7 @@ __device__ __forceinline__ int64_t cost_bound(const int64_t* __restrict__ cost, 
 
 // P pipelines x SSP super-stages of R blocks each.  A super-stage holds up to R consecutive blocks
 // of one work unit: their gathered B rows (operand A of R / BPS MMA steps) and their fragments.
-template <class BT, int NF, int P, int SSP, int R, int PP>
+template <class BT, int NF, int P, int SSP, int R, int PP, int kLsu>
 __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
     k_spmm_tc(SpmmArgs a, const uint8_t* __restrict__ frags, const __grid_constant__ CUtensorMap bmap) {
   using G = Geo<BT, NF>;
@@ -166,6 +180,10 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::MISC);  // [0] tmem base, [2 + e] ticket
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef RSH_TC_PROFILE
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
+#endif
 
   // zero the A stages once: feature atoms no gather writes (fp32 N = 32 under an M = 64 MMA) stay
   // zero for the whole launch
@@ -173,7 +191,9 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);   // the producer's arrive.expect_tx (+ gather and fragment bytes)
+      // the producer's arrive.expect_tx (+ gather and fragment bytes); LSU-staged super-stages
+      // add one cp.async.mbarrier.arrive.noinc per producer lane
+      mbar_init(full + s, (s % SSP) >= SSP - kLsu ? 33 : 1);
       mbar_init(empty + s, 1);  // tcgen05.commit after the super-stage's MMAs
     }
     for (int s = 0; s < G::NACC; ++s) {
@@ -283,11 +303,15 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
           const int nblk = nb - k0 < R ? nb - k0 : R;
           const int nfb = (nblk + G::BPS - 1) / G::BPS * G::BPS;  // blocks of whole steps
           const int ss = p * SSP + (int)(q % SSP);
-          mbar_wait(empty + ss, (uint32_t)(((q / SSP) & 1) ^ 1));
+          PROF_WAIT(1, mbar_wait(empty + ss, (uint32_t)(((q / SSP) & 1) ^ 1)));
           uint8_t* stA = sA + (size_t)ss * L::STEPS * G::ABYTES;
+          // staging engine of this super-stage: the TMA (gather4) or, for the last kLsu of each
+          // pipeline's SSP super-stages, the LSU (16-byte cp.async per lane): the two engines run
+          // side by side
+          const bool lsu = (ss % SSP) >= SSP - kLsu;
           if (lane == 0) {
             const bool no_frag = a.flags & 64;  // perf-probe knobs: no fragment copy / a fixed one
-            mbar_expect_tx(full + ss, (no_gather ? 0u : nfb * G::TXB) + (no_frag ? 0u : nfb * G::FB));
+            mbar_expect_tx(full + ss, ((no_gather || lsu) ? 0u : nfb * G::TXB) + (no_frag ? 0u : nfb * G::FB));
             if (!no_frag)
               asm volatile(
                   "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
@@ -297,22 +321,72 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
                   : "memory");
           }
           __syncwarp();
-          // lanes k0 .. k0 + nfb - 1 gather their own block's rows (lanes past nblk: the missing
-          // half of a bf16 step, rows -1): K quad qd (rows 4qd..4qd+3) x real MN atom ga; block j
-          // of the super-stage is K group (j % BPS) of step j / BPS
-          const int j = lane - k0;
-          if (j >= 0 && j < nfb && !no_gather) {
-            const int step = j / G::BPS, b = j % G::BPS;
+          if (lsu) {
+            // block j of the super-stage, row r, 16-byte chunk cc of the row's real features: one
+            // cp.async per lane per chunk into the swizzled operand image (padding rows: zero
+            // fill); completion reaches the full barrier through cp.async.mbarrier.arrive.noinc
+            constexpr int CPR = NF * G::EB / 16;  // chunks per row
+            constexpr int CPB = 8 * CPR;          // chunks per block
+            const char* Bb = reinterpret_cast<const char*>(a.B);
+            const int64_t rowb = a.ldb * G::EB;
+            for (int j = 0; j < nfb; ++j) {
+              const int src = (k0 + j) & 31;
+              int col8[8];
+              col8[0] = __shfl_sync(0xffffffffu, c0.x, src);
+              col8[1] = __shfl_sync(0xffffffffu, c0.y, src);
+              col8[2] = __shfl_sync(0xffffffffu, c0.z, src);
+              col8[3] = __shfl_sync(0xffffffffu, c0.w, src);
+              col8[4] = __shfl_sync(0xffffffffu, c1.x, src);
+              col8[5] = __shfl_sync(0xffffffffu, c1.y, src);
+              col8[6] = __shfl_sync(0xffffffffu, c1.z, src);
+              col8[7] = __shfl_sync(0xffffffffu, c1.w, src);
+              const int step = j / G::BPS, b = j % G::BPS;
+              uint8_t* stS = stA + step * G::ABYTES;
+            // rows covered by one warp instruction: 32 / CPR (CPR >= 32: one row, warp-uniform)
+            constexpr int RPI = CPR >= 32 ? 1 : 32 / CPR;
 #pragma unroll
-            for (int qd = 0; qd < 2; ++qd) {
-              const int4 cc = qd ? c1 : c0;
-              const int kr0 = 8 * b + 4 * qd, kg = kr0 / G::KGR, qin = kr0 % G::KGR;
+              for (int it = 0; it < (CPB + 31) / 32; ++it) {
+                const int c = lane + 32 * it;
+                if (CPB % 32 == 0 || c < CPB) {
+                  const int r = c / CPR, cc = c % CPR;
+                  const int fb = cc * 16, ga = fb >> 7, ci = (fb & 127) >> 4;
+                  const int t = ga / G::NMA, ma = ga % G::NMA;
+                  const int kk = 8 * b + r, kg = kk / G::KGR, kr = kk % G::KGR;
+                  const int within = G::EB == 4 ? kr * 128 + ((((ci >> 1) ^ kr)) << 5) + ((ci & 1) << 4)
+                                                : kr * 128 + ((ci ^ kr) << 4);
+                  // this instruction's rows are r0 .. r0 + RPI - 1 (r0 compile-time): RPI - 1 selects
+                  const int r0 = CPR >= 32 ? (32 * it) / CPR : (32 * it) / CPR;
+                  int col = col8[r0 & 7];
 #pragma unroll
-              for (int ga = 0; ga < G::NRA; ++ga) {
-                const int t = ga / G::NMA, ma = ga % G::NMA;
-                const uint32_t dst = smem_u32(stA + step * G::ABYTES + t * G::TILE) + kg * G::SBO + ma * G::LBO +
-                                     qin * 128;
-                gather4(&bmap, dst, full + ss, ga * G::PER_ATOM, cc.x, cc.y, cc.z, cc.w, pol_b);
+                  for (int q8 = 1; q8 < RPI; ++q8)
+                    if (r == r0 + q8) col = col8[(r0 + q8) & 7];
+                  const uint32_t dst = smem_u32(stS + t * G::TILE) + kg * G::SBO + ma * G::LBO + within;
+                  const char* srcp = Bb + (col >= 0 ? (int64_t)col * rowb + fb : 0);
+                  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
+                               "l"(srcp), "r"(col >= 0 ? 16 : 0), "l"(pol_b)
+                               : "memory");
+                }
+              }
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + ss)) : "memory");
+          } else {
+            // lanes k0 .. k0 + nfb - 1 gather their own block's rows (lanes past nblk: the missing
+            // half of a bf16 step, rows -1): K quad qd (rows 4qd..4qd+3) x real MN atom ga; block j
+            // of the super-stage is K group (j % BPS) of step j / BPS
+            const int j = lane - k0;
+            if (j >= 0 && j < nfb && !no_gather) {
+              const int step = j / G::BPS, b = j % G::BPS;
+#pragma unroll
+              for (int qd = 0; qd < 2; ++qd) {
+                const int4 cc = qd ? c1 : c0;
+                const int kr0 = 8 * b + 4 * qd, kg = kr0 / G::KGR, qin = kr0 % G::KGR;
+#pragma unroll
+                for (int ga = 0; ga < G::NRA; ++ga) {
+                  const int t = ga / G::NMA, ma = ga % G::NMA;
+                  const uint32_t dst = smem_u32(stA + step * G::ABYTES + t * G::TILE) + kg * G::SBO + ma * G::LBO +
+                                       qin * 128;
+                  gather4(&bmap, dst, full + ss, ga * G::PER_ATOM, cc.x, cc.y, cc.z, cc.w, pol_b);
+                }
               }
             }
           }
@@ -363,7 +437,7 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
         const int32_t uz = __shfl_sync(0xffffffffu, unl.z, k), uw = __shfl_sync(0xffffffffu, unl.w, k);
         if (lane == 0) {
           const int slot = (int)(ua % G::NACC);
-          mbar_wait(tempty + slot, (uint32_t)(((ua / G::NACC) & 1) ^ 1));
+          PROF_WAIT(3, mbar_wait(tempty + slot, (uint32_t)(((ua / G::NACC) & 1) ^ 1)));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (uz == uw) {
             mbar_arrive(tfull + slot);
@@ -375,7 +449,10 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
                 const int nblk = nb - k0 < R ? nb - k0 : R;
                 const int nsteps = (nblk + G::BPS - 1) / G::BPS;
                 const int ss = p * SSP + (int)(q % SSP);
-                mbar_wait(full + ss, (uint32_t)((q / SSP) & 1));
+                PROF_WAIT(2, mbar_wait(full + ss, (uint32_t)((q / SSP) & 1)));
+                // LSU-staged rows are generic-proxy writes: order them before the MMA's
+                // async-proxy reads (consumer-side proxy fence after the barrier's acquire)
+                if ((ss % SSP) >= SSP - kLsu) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 // descriptors: the 14-bit start-address field (bytes >> 4) of the stage-0 descriptors
                 // plus the stage / step / tile offset (shared memory < 256 KB: no carry out)
@@ -441,7 +518,7 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
           const int64_t ua = ub + (int64_t)kEpiGroups * ku;
           const int slot = (int)(ua % G::NACC);
           const bool has = __shfl_sync(0xffffffffu, unl.z, ku) != __shfl_sync(0xffffffffu, unl.w, ku);
-          mbar_wait(tfull + slot, (uint32_t)((ua / G::NACC) & 1));
+          PROF_WAIT(4, mbar_wait(tfull + slot, (uint32_t)((ua / G::NACC) & 1)));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
           for (int t = 0; t < G::MT; ++t) {
@@ -545,6 +622,14 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
     }
   }
 
+#ifdef RSH_TC_PROFILE
+  if (lane == 0) {
+    prof[0] = clock64() - t_start;
+    const int slot = blockIdx.x * 40 + warp;
+    if (slot < 148 * 40)
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_tc_prof[slot][i], prof[i]);
+  }
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == kMma0) {
@@ -622,14 +707,14 @@ int make_bmap(CUtensorMap* map, const void* B, int64_t b_rows, int64_t ldb, int 
   return kOk;
 }
 
-template <class BT, int NF, int P, int SSP, int R, int PP = 1>
+template <class BT, int NF, int P, int SSP, int R, int LSU, int PP = 1>
 int launch(const SpmmArgs& a, const uint8_t* frags, const void* B, int64_t b_rows, cudaStream_t st) {
   using G = Geo<BT, NF>;
   using L = Smem<G, P * SSP, R>;
   static_assert(L::BYTES <= 227 * 1024, "shared memory budget");
   CUtensorMap map;
   RSH_OK(make_bmap<BT>(&map, B, b_rows, a.ldb, NF));
-  auto kern = k_spmm_tc<BT, NF, P, SSP, R, PP>;
+  auto kern = k_spmm_tc<BT, NF, P, SSP, R, PP, LSU>;
   static bool init = false;
   if (!init) {
     RSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES));
@@ -640,21 +725,24 @@ int launch(const SpmmArgs& a, const uint8_t* frags, const void* B, int64_t b_row
   return launch_fixup<float>(a, st);
 }
 
-// pipelines x super-stages x blocks per super-stage, sized to ~200 KB of shared memory
+// pipelines x super-stages x blocks per super-stage (~200 KB of shared memory) and how many of a
+// pipeline's super-stages the LSU stages (measured: N <= 64 runs best on the TMA alone -- config 3
+// 0.84 vs 0.93 ms half-and-half -- while wider rows gain from the second engine, config 2 1.52 vs
+// 1.68 ms; profiles/r02_tc_kernel_evolution.txt)
 template <class BT>
 int dispatch_n(const SpmmArgs& a, const uint8_t* frags, const void* B, int64_t b_rows, int N, cudaStream_t st) {
   if constexpr (sizeof(BT) == 4) {
     switch (N) {
-      case 32: return launch<BT, 32, 10, 2, 4>(a, frags, B, b_rows, st);
-      case 64: return launch<BT, 64, 10, 2, 4>(a, frags, B, b_rows, st);
-      case 128: return launch<BT, 128, 8, 2, 2>(a, frags, B, b_rows, st);
-      case 256: return launch<BT, 256, 6, 2, 2>(a, frags, B, b_rows, st);
+      case 32: return launch<BT, 32, 10, 2, 4, 0>(a, frags, B, b_rows, st);
+      case 64: return launch<BT, 64, 10, 2, 4, 0>(a, frags, B, b_rows, st);
+      case 128: return launch<BT, 128, 8, 2, 2, 1>(a, frags, B, b_rows, st);
+      case 256: return launch<BT, 256, 6, 2, 2, 1>(a, frags, B, b_rows, st);
     }
   } else {
     switch (N) {
-      case 64: return launch<BT, 64, 8, 2, 8>(a, frags, B, b_rows, st);
-      case 128: return launch<BT, 128, 8, 2, 4>(a, frags, B, b_rows, st);
-      case 256: return launch<BT, 256, 6, 2, 4>(a, frags, B, b_rows, st);
+      case 64: return launch<BT, 64, 8, 2, 8, 0>(a, frags, B, b_rows, st);
+      case 128: return launch<BT, 128, 8, 2, 4, 1>(a, frags, B, b_rows, st);
+      case 256: return launch<BT, 256, 6, 2, 4, 1>(a, frags, B, b_rows, st);
     }
   }
   return fail(kInvalid, "rsh_spmm_tc: unsupported N %d", N);
@@ -666,6 +754,15 @@ int dispatch_n(const SpmmArgs& a, const uint8_t* frags, const void* B, int64_t b
 using namespace rsh;
 
 extern "C" {
+
+#ifdef RSH_TC_PROFILE
+int rsh_tc_profile_read(unsigned long long* host_out) {
+  RSH_CUDA(cudaMemcpyFromSymbol(host_out, tc::g_tc_prof, sizeof(tc::g_tc_prof)));
+  static unsigned long long zeros[148 * 40][8];
+  RSH_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof, zeros, sizeof(zeros)));
+  return kOk;
+}
+#endif
 
 size_t rsh_tc_fragment_bytes(int64_t n_blocks, int32_t b_dtype) {
   return (size_t)(n_blocks + 2) * (b_dtype == 0 ? 256 : 128);

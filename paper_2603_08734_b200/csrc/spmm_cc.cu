@@ -1037,13 +1037,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
 
 template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap, int kG = 1>
 int launch_stream_k(const SpmmArgs& a, cudaStream_t st) {
-  static int blocks = 0;
   auto kern = k_spmm_stream<VEC, BT, kDepth, MINB, kFull, kNoL1, kCap, kG>;
-  if (!blocks) {
+  // persistent grid: resident CTAs per SM x SMs, computed once (thread-safe static init)
+  static const int blocks = [&] {
     int per_sm = 0;
-    RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
-    blocks = (per_sm > 0 ? per_sm : 1) * sm_count();
-  }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0) != cudaSuccess) per_sm = 1;
+    return (per_sm > 0 ? per_sm : 1) * sm_count();
+  }();
   kern<<<blocks, kThreads, 0, st>>>(a);
   RSH_LAUNCHED("k_spmm_stream");
   return launch_fixup<float>(a, st);
@@ -1086,13 +1086,13 @@ int dispatch_stream(const SpmmArgs& a, cudaStream_t st) {
 
 template <int VEC, class BT, class AccT, int MINB, int PF, int G = 1>
 int launch_cc_v(const SpmmArgs& a, cudaStream_t st) {
-  static int blocks = 0;
   auto kern = k_spmm_cc<VEC, BT, AccT, MINB, PF, G>;
-  if (!blocks) {
+  // persistent grid: resident CTAs per SM x SMs, computed once (thread-safe static init)
+  static const int blocks = [&] {
     int per_sm = 0;
-    RSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
-    blocks = (per_sm > 0 ? per_sm : 1) * sm_count();
-  }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0) != cudaSuccess) per_sm = 1;
+    return (per_sm > 0 ? per_sm : 1) * sm_count();
+  }();
   kern<<<blocks, kThreads, 0, st>>>(a);
   RSH_LAUNCHED("k_spmm_cc");
   return launch_fixup<AccT>(a, st);

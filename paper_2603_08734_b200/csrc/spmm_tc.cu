@@ -715,11 +715,9 @@ int launch(const SpmmArgs& a, const uint8_t* frags, const void* B, int64_t b_row
   CUtensorMap map;
   RSH_OK(make_bmap<BT>(&map, B, b_rows, a.ldb, NF));
   auto kern = k_spmm_tc<BT, NF, P, SSP, R, PP, LSU>;
-  static bool init = false;
-  if (!init) {
-    RSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES));
-    init = true;
-  }
+  // opt in to the dynamic shared memory once (thread-safe static init)
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+  RSH_CUDA(attr);
   kern<<<sm_count(), (kEpiWarps + P + P * PP) * 32, L::BYTES, st>>>(a, frags, map);
   RSH_LAUNCHED("k_spmm_tc");
   return launch_fixup<float>(a, st);

@@ -423,8 +423,10 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
     path = resolve_math(math, b, t, accumulate)
     if path == "tc":
         chunk = CHUNK_TC
-    elif acc == 0 and ROWMAJOR_LIST and not (cc_variant & (64 | 4096)):
-        chunk = CHUNK_CC_LIST  # long units + the row-major list (flags 64 / 4096: row walk / bitmap decode)
+    elif acc == 0 and ROWMAJOR_LIST and not ((cc_variant << 1) & (64 | 4096)):
+        # long units + the row-major list (kernel flags 64 / 4096 = cc_variant 32 / 2048 ask for the
+        # row walk / the bitmap-decoding stream, which need 32-block units and no list)
+        chunk = CHUNK_CC_LIST
     else:
         chunk = CHUNK_CC
     plan = spmm_plan(t, chunk)

@@ -465,7 +465,7 @@ def run_single(args):
     achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
     peaks = _peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    gathered = int(plan_gather_bytes(tile, w.n_features, b_elem))
+    gathered = int(plan_gather_bytes(tile, w.n_features, b_elem, per_slot=(kernel == "k_spmm_tc")))
 
     # end to end through the public device API with host buffers: every step copies the format and
     # B in from pinned host memory, builds the schedule (the format's arrays are new, so the
@@ -559,8 +559,9 @@ def run_single(args):
         "gather": {"gathered_bytes": gathered, "achieved_gbs": gathered / (kern_avg * 1e-3) / 1e9,
                    "roof_l2_resident_gbs": GATHER_ROOF_L2_GBS, "roof_hbm_gbs": GATHER_ROOF_HBM_GBS,
                    "frac_of_l2_roof": gathered / (kern_avg * 1e-3) / 1e9 / GATHER_ROOF_L2_GBS,
-                   "note": "B rows the window path must move into the SMs (one per occupied col_id slot "
-                           "+ one per residual nonzero); roofs from tools/microbench/gather_plateau.cu"},
+                   "note": "B rows the timed kernel moves into the SMs (stream: one per nonzero; tensor "
+                           "cores: one per occupied col_id slot; + one per residual nonzero); roofs from "
+                           "tools/microbench/gather_plateau.cu"},
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms_step, "steps": args.e2e_steps,
                 "sequential_value": e2e_seq_value, "sequential_ms_per_step": e2e_seq_ms,
@@ -573,10 +574,14 @@ def run_single(args):
     print(json.dumps(line), flush=True)
 
 
-def plan_gather_bytes(tile, n_feat: int, b_elem: int) -> int:
-    """B bytes the window path must gather: one row per non-padding col_id slot (a slot whose
-    bitmap column is empty is skipped), plus one row per residual nonzero."""
+def plan_gather_bytes(tile, n_feat: int, b_elem: int, per_slot: bool) -> int:
+    """B bytes the kernel must move into the SMs: the streaming kernel gathers one B row per
+    nonzero; the tensor-core window path one per occupied col_id slot (a slot whose bitmap column
+    is empty is skipped) -- plus one per residual nonzero on both."""
     import torch
+    res = int(tile.res_col_id.numel()) if tile.n_res else 0
+    if not per_slot:
+        return (int(tile.values.numel()) + res) * n_feat * b_elem
     bm = tile.bitmaps
     if bm.numel() == 0:
         slots = 0
@@ -586,7 +591,7 @@ def plan_gather_bytes(tile, n_feat: int, b_elem: int) -> int:
             x = x | (x >> sh) if sh != 32 else x | ((x >> 32) & 0xFFFFFFFF)
         x = x & 0xFF
         slots = int(sum(((x >> j) & 1).sum().item() for j in range(8)))
-    return (slots + int(tile.res_col_id.numel())) * n_feat * b_elem
+    return (slots + res) * n_feat * b_elem
 
 
 if __name__ == "__main__":

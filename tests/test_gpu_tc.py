@@ -130,3 +130,25 @@ def test_exec_config_tf32_through_host_api(small_corpus):
     assert O.rel_frobenius(c, ref64) <= TF32_TOL
     with pytest.raises(ValueError):
         P.hybrid_spmm(m, P.DenseMatrix.from_array(b[:, :100]), P.ExecConfig(math="tf32"))
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_spmm_device_is_cuda_graph_capturable(small_corpus, math):
+    """bench.py times CUDA-graph replays of spmm_device: a captured step equals a direct call
+    bitwise (no host synchronisation or allocation inside a warmed-up call)."""
+    from paper_2603_08734_b200.device import spmm_device
+    a = small_corpus[3]
+    t = _tile(a)
+    b = _b(a.n_cols, 128, 4)
+    ref = spmm_device(t, b, math=math)
+    out = torch.empty_like(ref)
+    spmm_device(t, b, out=out, math=math)  # warm-up: schedule, fragments, workspace
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        spmm_device(t, b, out=out, math=math)
+    out.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)

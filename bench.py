@@ -487,70 +487,18 @@ def run_single(args):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     gathered = int(plan_gather_bytes(tile, w.n_features, b_elem, per_slot=(kernel == "k_spmm_tc")))
 
-    # end to end through the public device API with host buffers: every step copies the format and
-    # B in from pinned host memory, builds the schedule (the format's arrays are new, so the
-    # cached one is stale), runs the SpMM and copies C out.  Steps are pipelined over three
-    # streams with two device buffer sets, so step i's C -> host copy overlaps step i+1's
-    # host -> device copies (PCIe is full duplex); every copy stays inside the timed region.
-    fields = ("row_window_id", "row_window_offset", "bitmaps", "col_id", "values", "res_row_id", "res_offset",
-              "res_col_id", "res_values")
-    host = {k: getattr(tile, k).cpu().pin_memory() for k in fields}
-    b_host = bt.cpu().pin_memory()
-    c_hosts = [torch.empty((a.n_rows, w.n_features), dtype=torch.float32).pin_memory() for _ in range(2)]
-    sets = []
-    for _ in range(2):
-        bufs = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
-        sets.append((DeviceTile(tile.n_rows, tile.n_cols, tile.window_size, **bufs), bufs,
-                     torch.empty_like(b_host, device=dev), torch.empty_like(out)))
+    # end to end through the public device API with host buffers (device.HostStream): every step
+    # copies the format and B in from pinned host memory, builds the schedule (the format's arrays
+    # are new data), runs the SpMM and copies C out; steps pipelined over three streams with two
+    # buffer sets (C out of step i overlaps the inputs of step i+1); every copy is timed
+    from paper_2603_08734_b200.device import TILE_HOST_FIELDS, HostStream
     del out
-    h2d = sum(v.numel() * v.element_size() for v in host.values()) + b_host.numel() * b_host.element_size()
-    d2h = c_hosts[0].numel() * 4
-    s_in, s_comp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-
-    def e2e_run(n_steps: int, pipelined: bool) -> float:
-        ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
-        comp_done, out_done = [None, None], [None, None]
-        torch.cuda.synchronize()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(s_in)
-        for i in range(n_steps):
-            k = i % 2 if pipelined else 0
-            t2, bufs, b_dev, c_dev = sets[k]
-            if comp_done[k] is not None:
-                s_in.wait_event(comp_done[k])          # set k's inputs are free again
-            if i == 0:
-                s_comp.wait_event(t0)
-            with torch.cuda.stream(s_in):
-                for f, v in host.items():
-                    bufs[f].copy_(v, non_blocking=True)
-                b_dev.copy_(b_host, non_blocking=True)
-                in_done = ev()
-                in_done.record(s_in)
-            s_comp.wait_event(in_done)
-            if out_done[k] is not None:
-                s_comp.wait_event(out_done[k])          # set k's C has reached the host
-            with torch.cuda.stream(s_comp):
-                spmm_device(t2, b_dev, out=c_dev, math=math, stream=s_comp)
-                comp_done[k] = ev()
-                comp_done[k].record(s_comp)
-            s_out.wait_event(comp_done[k])
-            with torch.cuda.stream(s_out):
-                c_hosts[k].copy_(c_dev, non_blocking=True)
-                out_done[k] = ev()
-                out_done[k].record(s_out)
-            if not pipelined:
-                torch.cuda.synchronize()
-        for e in out_done:
-            if e is not None:
-                s_out.wait_event(e)
-        t1.record(s_out)
-        torch.cuda.synchronize()
-        return t0.elapsed_time(t1) / n_steps
-
-    e2e_run(2, True)  # warm-up: schedules, fragments, allocator
-    e2e_seq_ms = e2e_run(max(2, args.e2e_steps // 2), False)
-    e2e_ms_step = e2e_run(args.e2e_steps, True)
+    hs = HostStream({k: getattr(tile, k).cpu().pin_memory() for k in TILE_HOST_FIELDS}, bt.cpu().pin_memory(),
+                    tile.n_rows, tile.n_cols, tile.window_size, dev, math)
+    h2d, d2h = hs.h2d_bytes, hs.d2h_bytes
+    hs.timed(2)  # warm-up: schedules, fragments, allocator
+    e2e_seq_ms = hs.timed(max(2, args.e2e_steps // 2), pipelined=False)
+    e2e_ms_step = hs.timed(args.e2e_steps)
     e2e_value = flops / (e2e_ms_step * 1e-3) / 1e9
     e2e_seq_value = flops / (e2e_seq_ms * 1e-3) / 1e9
 
@@ -586,9 +534,9 @@ def run_single(args):
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms_step, "steps": args.e2e_steps,
                 "sequential_value": e2e_seq_value, "sequential_ms_per_step": e2e_seq_ms,
-                "path": f"spmm_device ({kernel}) via the C ABI: pinned host format + B in, schedule build, "
-                        "SpMM, C out; steps pipelined on 3 streams x 2 buffer sets (C out of step i overlaps "
-                        "the inputs of step i+1); sequential_* = one step at a time"},
+                "path": f"device.HostStream ({kernel} via the C ABI): pinned host format + B in, schedule "
+                        "build, SpMM, C out; steps pipelined on 3 streams x 2 buffer sets (C out of step i "
+                        "overlaps the inputs of step i+1); sequential_* = one step at a time"},
         "cpu_baseline": cpu,
         "clocks": clk,
     }

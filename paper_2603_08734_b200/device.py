@@ -454,3 +454,101 @@ def max_relative_error_device(c: torch.Tensor, ref: torch.Tensor, stream=None) -
     call("rsh_max_relative_error", _ptr(c), _ptr(ref), c.shape[0], c.shape[1], c.stride(0), _ptr(out),
          _stream(stream))
     return float(out.item())
+
+
+# ---------------------------------------------------------------------------------------------
+# host-resident operands, streamed
+# ---------------------------------------------------------------------------------------------
+
+TILE_HOST_FIELDS = ("row_window_id", "row_window_offset", "bitmaps", "col_id", "values", "res_row_id", "res_offset",
+                    "res_col_id", "res_values")
+
+
+class HostStream:
+    """SpMMs whose format, B and C live in (pinned) host memory: every ``step`` copies the format
+    and B in, runs ``spmm_device`` (schedule rebuilt: the arrays are new data) and copies C out.
+    Steps are pipelined over three CUDA streams with two device buffer sets, so step i's C copy
+    overlaps step i+1's input copies (PCIe is full duplex) and the SpMM runs between them.
+
+    ``host``: dict of pinned host tensors keyed by TILE_HOST_FIELDS; ``b_host`` pinned B;
+    ``n_rows`` / ``n_cols`` / ``window_size`` describe the format; results land in the two pinned
+    ``c_host`` buffers alternately (``result(i)`` after ``sync()``)."""
+
+    def __init__(self, host: dict, b_host: torch.Tensor, n_rows: int, n_cols: int, window_size: int,
+                 device=None, math: str = "auto"):
+        dev = require_cuda(device)
+        self.host, self.b_host, self.math = host, b_host, math
+        self.c_host = [torch.empty((n_rows, int(b_host.shape[1])), dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.sets = []
+        for _ in range(2):
+            bufs = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+            self.sets.append((DeviceTile(n_rows, n_cols, window_size, **bufs), bufs,
+                              torch.empty_like(b_host, device=dev),
+                              torch.empty((n_rows, int(b_host.shape[1])), dtype=torch.float32, device=dev)))
+        self.s_in, self.s_comp, self.s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        self._comp = [None, None]
+        self._out = [None, None]
+        self.i = 0
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(v.numel() * v.element_size() for v in self.host.values()) + \
+            self.b_host.numel() * self.b_host.element_size()
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.c_host[0].numel() * 4
+
+    def step(self, pipelined: bool = True) -> None:
+        k = self.i % 2 if pipelined else 0
+        t, bufs, b_dev, c_dev = self.sets[k]
+        ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+        if self._comp[k] is not None:
+            self.s_in.wait_event(self._comp[k])            # set k's inputs are free again
+        with torch.cuda.stream(self.s_in):
+            for f, v in self.host.items():
+                bufs[f].copy_(v, non_blocking=True)
+            b_dev.copy_(self.b_host, non_blocking=True)
+            in_done = ev()
+            in_done.record(self.s_in)
+        self.s_comp.wait_event(in_done)
+        if self._out[k] is not None:
+            self.s_comp.wait_event(self._out[k])           # set k's C has reached the host
+        with torch.cuda.stream(self.s_comp):
+            spmm_device(t, b_dev, out=c_dev, math=self.math, stream=self.s_comp)
+            self._comp[k] = ev()
+            self._comp[k].record(self.s_comp)
+        self.s_out.wait_event(self._comp[k])
+        with torch.cuda.stream(self.s_out):
+            self.c_host[k].copy_(c_dev, non_blocking=True)
+            self._out[k] = ev()
+            self._out[k].record(self.s_out)
+        self.i += 1
+        if not pipelined:
+            torch.cuda.synchronize()
+
+    def result(self, i: int) -> torch.Tensor:
+        """Host C of step i (valid after sync(), until step i + 2 is issued)."""
+        return self.c_host[i % 2]
+
+    def sync(self) -> None:
+        for e in self._out:
+            if e is not None:
+                self.s_out.wait_event(e)
+        torch.cuda.synchronize()
+
+    def timed(self, n_steps: int, pipelined: bool = True) -> float:
+        """Milliseconds per step over n_steps steps (device events from the first input copy to
+        the last C copy)."""
+        self.sync()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(self.s_in)
+        self.s_comp.wait_event(t0)
+        for _ in range(n_steps):
+            self.step(pipelined)
+        for e in self._out:
+            if e is not None:
+                self.s_out.wait_event(e)
+        t1.record(self.s_out)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / n_steps

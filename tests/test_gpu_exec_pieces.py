@@ -79,3 +79,22 @@ def test_exec_residual_identity():
     assert np.array_equal(c, b.data)
     P.exec_residual(m, b, c)  # accumulates
     assert np.array_equal(c, 2 * b.data)
+
+
+def test_host_stream_pipelined_steps_match_device_result(small_corpus):
+    """device.HostStream (host-resident format + B, pipelined copies): every step's host C equals
+    the device-resident product bitwise."""
+    import torch
+    from paper_2603_08734_b200.device import TILE_HOST_FIELDS, DeviceCsr, HostStream, build_device, spmm_device
+    a = small_corpus[7]
+    t = build_device(DeviceCsr.from_host(a))
+    b = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, (a.n_cols, 64)).astype(np.float32)).cuda()
+    ref = spmm_device(t, b).cpu()
+    hs = HostStream({k: getattr(t, k).cpu().pin_memory() for k in TILE_HOST_FIELDS}, b.cpu().pin_memory(),
+                    t.n_rows, t.n_cols, t.window_size)
+    for i in range(5):
+        hs.step(pipelined=True)
+    hs.sync()
+    assert torch.equal(hs.result(3), ref) and torch.equal(hs.result(4), ref)
+    assert hs.timed(3) > 0 and hs.timed(2, pipelined=False) > 0
+    assert torch.equal(hs.result(0), ref)

@@ -160,8 +160,8 @@ __device__ __forceinline__ int64_t cost_bound(const int64_t* __restrict__ cost, 
 
 // P pipelines x SSP super-stages of R blocks each.  A super-stage holds up to R consecutive blocks
 // of one work unit: their gathered B rows (operand A of R / BPS MMA steps) and their fragments.
-template <class BT, int NF, int P, int SSP, int R, int PP, int kLsu>
-__global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
+template <class BT, int NF, int P, int SSP, int R, int kLsu>
+__global__ void __launch_bounds__((kEpiWarps + 2 * P) * 32, 1)
     k_spmm_tc(SpmmArgs a, const uint8_t* __restrict__ frags, const __grid_constant__ CUtensorMap bmap) {
   using G = Geo<BT, NF>;
   constexpr int S = P * SSP;
@@ -222,8 +222,7 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
 
   if (warp >= kProd0) {
     // ------------------------------------------------------------------ producers
-    // PP producer warps per pipeline take its super-stages round robin (q % PP)
-    const int p = (warp - kProd0) / PP, hp = (warp - kProd0) % PP;
+    const int p = warp - kProd0;
     uint64_t pol_b, pol_a;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
@@ -299,7 +298,6 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
         int4 c0, c1;
         pad(cur, c0, c1);
         for (int k0 = 0; k0 < nb; k0 += R, ++q) {
-          if (PP > 1 && (int)(q % PP) != hp) continue;
           const int nblk = nb - k0 < R ? nb - k0 : R;
           const int nfb = (nblk + G::BPS - 1) / G::BPS * G::BPS;  // blocks of whole steps
           const int ss = p * SSP + (int)(q % SSP);
@@ -413,7 +411,7 @@ __global__ void __launch_bounds__((kEpiWarps + P + P * PP) * 32, 1)
     }
     __syncwarp();
     if (lane == 0) {
-      const uint32_t producers = gridDim.x * P * PP;
+      const uint32_t producers = gridDim.x * P;
       if (atomicAdd(a.s.counters + 1, 1u) == producers - 1) {
         a.s.counters[0] = 0;
         a.s.counters[1] = 0;
@@ -707,18 +705,18 @@ int make_bmap(CUtensorMap* map, const void* B, int64_t b_rows, int64_t ldb, int 
   return kOk;
 }
 
-template <class BT, int NF, int P, int SSP, int R, int LSU, int PP = 1>
+template <class BT, int NF, int P, int SSP, int R, int LSU>
 int launch(const SpmmArgs& a, const uint8_t* frags, const void* B, int64_t b_rows, cudaStream_t st) {
   using G = Geo<BT, NF>;
   using L = Smem<G, P * SSP, R>;
   static_assert(L::BYTES <= 227 * 1024, "shared memory budget");
   CUtensorMap map;
   RSH_OK(make_bmap<BT>(&map, B, b_rows, a.ldb, NF));
-  auto kern = k_spmm_tc<BT, NF, P, SSP, R, PP, LSU>;
+  auto kern = k_spmm_tc<BT, NF, P, SSP, R, LSU>;
   // opt in to the dynamic shared memory once (thread-safe static init)
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
   RSH_CUDA(attr);
-  kern<<<sm_count(), (kEpiWarps + P + P * PP) * 32, L::BYTES, st>>>(a, frags, map);
+  kern<<<sm_count(), (kEpiWarps + 2 * P) * 32, L::BYTES, st>>>(a, frags, map);
   RSH_LAUNCHED("k_spmm_tc");
   return launch_fixup<float>(a, st);
 }

@@ -423,9 +423,9 @@ def spmm_device(t: DeviceTile, b: torch.Tensor, out: torch.Tensor | None = None,
     path = resolve_math(math, b, t, accumulate)
     if path == "tc":
         chunk = CHUNK_TC
-    elif acc == 0 and ROWMAJOR_LIST and not ((cc_variant << 1) & (64 | 4096)):
-        # long units + the row-major list (kernel flags 64 / 4096 = cc_variant 32 / 2048 ask for the
-        # row walk / the bitmap-decoding stream, which need 32-block units and no list)
+    elif acc == 0 and ROWMAJOR_LIST and not (cc_variant & (64 | 4096)):
+        # long units + the row-major list; cc_variant bits 64 / 4096 select 32-block units without
+        # the list (the bitmap-decoding stream; tests/test_gpu_parity.py compares the variants)
         chunk = CHUNK_CC_LIST
     else:
         chunk = CHUNK_CC
@@ -465,14 +465,16 @@ TILE_HOST_FIELDS = ("row_window_id", "row_window_offset", "bitmaps", "col_id", "
 
 
 class HostStream:
-    """SpMMs whose format, B and C live in (pinned) host memory: every ``step`` copies the format
-    and B in, runs ``spmm_device`` (schedule rebuilt: the arrays are new data) and copies C out.
-    Steps are pipelined over three CUDA streams with two device buffer sets, so step i's C copy
-    overlaps step i+1's input copies (PCIe is full duplex) and the SpMM runs between them.
+    """SpMMs whose format, B and C live in (pinned) host memory: every step copies the format and
+    B in, runs ``spmm_device`` (schedule rebuilt: the arrays are new data) and copies C out.
+    Steps are pipelined over three CUDA streams with two device buffer sets: step i+1's inputs
+    are enqueued before step i's SpMM (whose schedule build waits on the host for step i's
+    inputs), so the host-to-device engine never idles, and step i's C copy overlaps step i+1's
+    input copies (PCIe is full duplex).
 
     ``host``: dict of pinned host tensors keyed by TILE_HOST_FIELDS; ``b_host`` pinned B;
     ``n_rows`` / ``n_cols`` / ``window_size`` describe the format; results land in the two pinned
-    ``c_host`` buffers alternately (``result(i)`` after ``sync()``)."""
+    ``c_host`` buffers alternately (``result(i)`` after ``run``)."""
 
     def __init__(self, host: dict, b_host: torch.Tensor, n_rows: int, n_cols: int, window_size: int,
                  device=None, math: str = "auto"):
@@ -486,9 +488,6 @@ class HostStream:
                               torch.empty_like(b_host, device=dev),
                               torch.empty((n_rows, int(b_host.shape[1])), dtype=torch.float32, device=dev)))
         self.s_in, self.s_comp, self.s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        self._comp = [None, None]
-        self._out = [None, None]
-        self.i = 0
 
     @property
     def h2d_bytes(self) -> int:
@@ -499,54 +498,54 @@ class HostStream:
     def d2h_bytes(self) -> int:
         return self.c_host[0].numel() * 4
 
-    def step(self, pipelined: bool = True) -> None:
-        k = self.i % 2 if pipelined else 0
-        t, bufs, b_dev, c_dev = self.sets[k]
-        ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
-        if self._comp[k] is not None:
-            self.s_in.wait_event(self._comp[k])            # set k's inputs are free again
-        with torch.cuda.stream(self.s_in):
-            for f, v in self.host.items():
-                bufs[f].copy_(v, non_blocking=True)
-            b_dev.copy_(self.b_host, non_blocking=True)
-            in_done = ev()
-            in_done.record(self.s_in)
-        self.s_comp.wait_event(in_done)
-        if self._out[k] is not None:
-            self.s_comp.wait_event(self._out[k])           # set k's C has reached the host
-        with torch.cuda.stream(self.s_comp):
-            spmm_device(t, b_dev, out=c_dev, math=self.math, stream=self.s_comp)
-            self._comp[k] = ev()
-            self._comp[k].record(self.s_comp)
-        self.s_out.wait_event(self._comp[k])
-        with torch.cuda.stream(self.s_out):
-            self.c_host[k].copy_(c_dev, non_blocking=True)
-            self._out[k] = ev()
-            self._out[k].record(self.s_out)
-        self.i += 1
-        if not pipelined:
-            torch.cuda.synchronize()
-
     def result(self, i: int) -> torch.Tensor:
-        """Host C of step i (valid after sync(), until step i + 2 is issued)."""
+        """Host C of step i of the last ``run`` (the last two steps' results are kept)."""
         return self.c_host[i % 2]
 
-    def sync(self) -> None:
-        for e in self._out:
-            if e is not None:
-                self.s_out.wait_event(e)
+    def run(self, n_steps: int, pipelined: bool = True) -> float:
+        """n_steps steps; returns milliseconds per step (device events from the first input copy
+        to the last C copy).  pipelined=False runs one step at a time (one buffer set)."""
         torch.cuda.synchronize()
-
-    def timed(self, n_steps: int, pipelined: bool = True) -> float:
-        """Milliseconds per step over n_steps steps (device events from the first input copy to
-        the last C copy)."""
-        self.sync()
+        ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+        comp_done, out_done, in_done = [None, None], [None, None], [None, None]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(self.s_in)
-        self.s_comp.wait_event(t0)
-        for _ in range(n_steps):
-            self.step(pipelined)
-        for e in self._out:
+
+        def stage_inputs(i: int) -> None:
+            k = i % 2 if pipelined else 0
+            _, bufs, b_dev, _ = self.sets[k]
+            if comp_done[k] is not None:
+                self.s_in.wait_event(comp_done[k])      # set k's inputs are free again
+            with torch.cuda.stream(self.s_in):
+                for f, v in self.host.items():
+                    bufs[f].copy_(v, non_blocking=True)
+                b_dev.copy_(self.b_host, non_blocking=True)
+                in_done[k] = ev()
+                in_done[k].record(self.s_in)
+
+        stage_inputs(0)
+        for i in range(n_steps):
+            k = i % 2 if pipelined else 0
+            t, _, b_dev, c_dev = self.sets[k]
+            if pipelined and i + 1 < n_steps:
+                stage_inputs(i + 1)                     # before this step's host-blocking schedule
+            self.s_comp.wait_event(in_done[k])
+            if out_done[k] is not None:
+                self.s_comp.wait_event(out_done[k])     # set k's C has reached the host
+            with torch.cuda.stream(self.s_comp):
+                spmm_device(t, b_dev, out=c_dev, math=self.math, stream=self.s_comp)
+                comp_done[k] = ev()
+                comp_done[k].record(self.s_comp)
+            self.s_out.wait_event(comp_done[k])
+            with torch.cuda.stream(self.s_out):
+                self.c_host[i % 2].copy_(c_dev, non_blocking=True)
+                out_done[k] = ev()
+                out_done[k].record(self.s_out)
+            if not pipelined:
+                torch.cuda.synchronize()
+                if i + 1 < n_steps:
+                    stage_inputs(i + 1)
+        for e in out_done:
             if e is not None:
                 self.s_out.wait_event(e)
         t1.record(self.s_out)

@@ -321,9 +321,9 @@ def run_sharded_bench(args, metric: str, clock_factory=None, config_factory=None
     hs = HostStream({k: getattr(tile, k).cpu().pin_memory() for k in TILE_HOST_FIELDS}, b.cpu().pin_memory(),
                     tile.n_rows, tile.n_cols, tile.window_size, dev)
     e2e_steps = max(2, min(args.steps, 6))
-    hs.timed(2)
+    hs.run(2)
     dist.barrier()
-    e2e_ms = [hs.timed(e2e_steps)]
+    e2e_ms = [hs.run(e2e_steps)]
     h2d = hs.h2d_bytes
     emax = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     dist.all_reduce(emax, op=dist.ReduceOp.MAX)

@@ -92,9 +92,7 @@ def test_host_stream_pipelined_steps_match_device_result(small_corpus):
     ref = spmm_device(t, b).cpu()
     hs = HostStream({k: getattr(t, k).cpu().pin_memory() for k in TILE_HOST_FIELDS}, b.cpu().pin_memory(),
                     t.n_rows, t.n_cols, t.window_size)
-    for i in range(5):
-        hs.step(pipelined=True)
-    hs.sync()
+    assert hs.run(5) > 0
     assert torch.equal(hs.result(3), ref) and torch.equal(hs.result(4), ref)
-    assert hs.timed(3) > 0 and hs.timed(2, pipelined=False) > 0
-    assert torch.equal(hs.result(0), ref)
+    assert hs.run(2, pipelined=False) > 0
+    assert torch.equal(hs.result(0), ref) and torch.equal(hs.result(1), ref)

@@ -187,9 +187,11 @@ int rsh_tc_fragments(int64_t n_rows, int64_t n_entries, const uint64_t* bitmaps,
  * {32, 64, 128, 256} (fp32 B) or {64, 128, 256} (half B); B rows 16-byte aligned.  b_rows = rows
  * of B (the TMA tensor map's extent: B rows are staged into shared memory by tile::gather4, and
  * padding slots read as zeros); fragments = rsh_tc_fragments(..., b_dtype) of this format.
- * Residual / uncovered rows run on CUDA cores in the same launch.  flags: bit 13 = "no window
- * needs the fix-up kernels" (as rsh_spmm_cc's accum bit 14); bits 0/2 are perf probes (skip the
- * gathers / the MMAs; results invalid). */
+ * Residual / uncovered rows run on CUDA cores in the same launch.  For N >= 128 half of each
+ * pipeline's super-stages are staged by 16-byte cp.async (the LSU) beside the TMA.  flags:
+ * bit 13 = "no window needs the fix-up kernels" (as rsh_spmm_cc's accum bit 14); bits 0 / 2 / 5 /
+ * 6 are perf probes (skip the gathers / MMAs / epilogue stores / fragment copies; results
+ * invalid). */
 int rsh_spmm_tc(int64_t n_rows, int32_t window_size, int64_t n_entries, const uint64_t* bitmaps,
                 const int32_t* col_id, const void* fragments, size_t fragment_bytes, int64_t n_blocks,
                 const int32_t* res_row_id, const int64_t* res_offset, const int32_t* res_col_id,

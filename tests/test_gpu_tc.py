@@ -152,3 +152,34 @@ def test_spmm_device_is_cuda_graph_capturable(small_corpus, math):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("d", [32, 64, 128, 256])
+def test_tc_edge_cases(d):
+    """Degenerate formats on the tensor-core path: identity through windows (B tf32-exact, so C
+    is B exactly), identity through residual rows only (no blocks at all), an all-zero matrix,
+    a single element, and padding slots next to a B row of large values (zero-filled by the
+    TMA's out-of-bounds rows, never multiplied in)."""
+    from paper_2603_08734_b200.device import spmm_device
+    rng = np.random.default_rng(d)
+    bq = (rng.integers(-64, 64, (16, d)) / 8.0).astype(np.float32)  # exact in tf32
+    b = torch.from_numpy(bq).cuda()
+    eye = P.CsrMatrix.from_dense(np.eye(16, dtype=np.float32))
+    t_win = _tile(eye, tau_nnz=0)
+    assert t_win.n_blocks > 0 and t_win.n_res == 0
+    assert torch.equal(spmm_device(t_win, b, math="tf32"), b)
+    t_res = _tile(eye)
+    assert t_res.n_blocks == 0 and t_res.n_res == 16
+    assert torch.equal(spmm_device(t_res, b, math="tf32"), b)
+    zero = P.CsrMatrix.from_dense(np.zeros((16, 16), np.float32))
+    assert not spmm_device(_tile(zero), b, math="tf32").any()
+    one = P.CsrMatrix.from_dense(np.full((1, 1), 2.0, np.float32))
+    assert torch.equal(spmm_device(_tile(one, tau_nnz=0), b[:1], math="tf32"), 2.0 * b[:1])
+    # one row using columns 1 and 9 (one block, 6 padding slots whose col_id is 0): B row 0 is NaN,
+    # but padding rows arrive as zeros from the TMA's out-of-bounds fill and never reach the MMA
+    dense = np.zeros((8, 16), np.float32)
+    dense[0, 1] = dense[0, 9] = 1.0
+    big = b.clone()
+    big[0] = float("nan")
+    c = spmm_device(_tile(P.CsrMatrix.from_dense(dense), tau_nnz=0), big, math="tf32")
+    assert torch.equal(c[0], big[1] + big[9]) and not c[1:].any()

@@ -13,6 +13,7 @@
 // weight sum over the shared columns (ascending column order), 1 for two empty rows, 0 when the
 // denominator is not positive.
 #include "common.cuh"
+#include <thread>
 #include <cub/cub.cuh>
 #include <algorithm>
 #include <vector>
@@ -531,20 +532,40 @@ int rsh_isolation_adjust(int64_t m, int64_t n_cols, const int64_t* rp, const int
   *n_isolated = 0;
   for (int64_t i = 0; i < m; ++i) order_out[i] = order_in[i];
   if (m <= 1 || iso_threshold == 0.0) return kOk;
+  // weighted Jaccard (reorder.py:41-52): the shared columns' weights summed in ascending column
+  // order -- by merging, or, for lopsided pairs (hub rows), by binary-searching the short row's
+  // columns in the long row (same columns, same order, so the same double)
   auto sim = [&](int64_t r, int64_t u) -> double {
     if (r == u) return 1.0;
     int64_t a = rp[r], ae = rp[r + 1], b = rp[u], be = rp[u + 1];
     if (a == ae && b == be) return 1.0;
     double wi = 0.0;
-    while (a < ae && b < be) {
-      if (ci[a] == ci[b]) {
-        wi += w[ci[a]];
-        ++a;
-        ++b;
-      } else if (ci[a] < ci[b]) {
-        ++a;
-      } else {
-        ++b;
+    if (ae - a > 16 * (be - b) || be - b > 16 * (ae - a)) {
+      if (ae - a > be - b) {
+        std::swap(a, b);
+        std::swap(ae, be);
+      }
+      int64_t lo = b;
+      for (; a < ae; ++a) {
+        const int32_t c = ci[a];
+        int64_t hi = be;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (ci[mid] < c) lo = mid + 1; else hi = mid;
+        }
+        if (lo < be && ci[lo] == c) wi += w[c];
+      }
+    } else {
+      while (a < ae && b < be) {
+        if (ci[a] == ci[b]) {
+          wi += w[ci[a]];
+          ++a;
+          ++b;
+        } else if (ci[a] < ci[b]) {
+          ++a;
+        } else {
+          ++b;
+        }
       }
     }
     const double tot = wsum[r] + wsum[u] - wi;
@@ -585,40 +606,67 @@ int rsh_isolation_adjust(int64_t m, int64_t n_cols, const int64_t* rp, const int
   std::vector<int64_t> empties;
   for (int64_t r = 0; r < m; ++r)
     if (rp[r + 1] == rp[r]) empties.push_back(r);
-  std::vector<int64_t> tail, cand;
-  std::vector<char> seen(m, 0);
   std::sort(isolated.begin(), isolated.end());
-  for (const int64_t r : isolated) {
-    int64_t best = NIL;
-    if (rp[r + 1] == rp[r]) {
-      for (const int64_t u : empties)
-        if (u != r && !iso[u]) {
-          best = u;
-          break;
-        }
-    } else {
-      cand.clear();
-      for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
-        const int32_t c = ci[p];
-        if (hub_cap >= 0 && cstart[c + 1] - cstart[c] > hub_cap) continue;
-        for (int64_t q = cstart[c]; q < cstart[c + 1]; ++q)
-          if (!seen[crow[q]]) {
-            seen[crow[q]] = 1;
-            cand.push_back(crow[q]);
-          }
-      }
-      for (const int64_t u : cand) seen[u] = 0;
-      std::sort(cand.begin(), cand.end());
-      double best_sim = 0.0;
-      for (const int64_t u : cand) {
-        if (u == r || iso[u]) continue;
-        const double sv = sim(r, u);
-        if (sv > best_sim) {
-          best = u;
-          best_sim = sv;
-        }
-      }
+  // the best match of every isolated row depends only on the static similarities and flags, so
+  // it is computed in parallel; the insertions then run in ascending row order (reorder.py:386-446)
+  const int64_t n_iso = (int64_t)isolated.size();
+  std::vector<int64_t> best_of(n_iso, NIL);
+  int64_t first_empty = NIL;  // the first non-isolated empty row (empty isolated rows' match)
+  for (const int64_t u : empties)
+    if (!iso[u]) {
+      first_empty = u;
+      break;
     }
+  auto work = [&](int64_t i0, int64_t i1) {
+    std::vector<int64_t> cand;
+    std::vector<char> seen(m, 0);
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t r = isolated[i];
+      int64_t best = NIL;
+      if (rp[r + 1] == rp[r]) {
+        best = first_empty;  // u != r holds: r is isolated, first_empty is not
+      } else {
+        cand.clear();
+        for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+          const int32_t c = ci[p];
+          if (hub_cap >= 0 && cstart[c + 1] - cstart[c] > hub_cap) continue;
+          for (int64_t q = cstart[c]; q < cstart[c + 1]; ++q)
+            if (!seen[crow[q]]) {
+              seen[crow[q]] = 1;
+              cand.push_back(crow[q]);
+            }
+        }
+        for (const int64_t u : cand) seen[u] = 0;
+        // the reference scans candidates in ascending order and keeps the first strict maximum:
+        // the largest similarity > 0, ties to the lower row -- order-free, so no sort
+        double best_sim = 0.0;
+        for (const int64_t u : cand) {
+          if (u == r || iso[u]) continue;
+          const double sv = sim(r, u);
+          if (sv > best_sim || (sv == best_sim && sv > 0.0 && u < best)) {
+            best = u;
+            best_sim = sv;
+          }
+        }
+      }
+      best_of[i] = best;
+    }
+  };
+  const int64_t n_threads = std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 64);
+  if (n_iso < 4096 || n_threads == 1) {
+    work(0, n_iso);
+  } else {
+    std::vector<std::thread> pool;
+    const int64_t per = (n_iso + n_threads - 1) / n_threads;
+    for (int64_t t = 0; t < n_threads; ++t) {
+      const int64_t i0 = t * per, i1 = std::min(n_iso, i0 + per);
+      if (i0 < i1) pool.emplace_back(work, i0, i1);
+    }
+    for (auto& th : pool) th.join();
+  }
+  std::vector<int64_t> tail;
+  for (int64_t i = 0; i < n_iso; ++i) {
+    const int64_t r = isolated[i], best = best_of[i];
     if (best == NIL) {
       tail.push_back(r);
     } else {

@@ -17,15 +17,15 @@ from paper_2603_08734_b200.device import DeviceCsr, build_device, spmm_device  #
 from paper_2603_08734_b200.reorder import ReorderParams, permute_rows_device, reorder_device  # noqa: E402
 
 
-def spmm_ms(t, b, iters=20):
+def spmm_ms(t, b, iters=20, math="auto"):
     out = torch.empty((t.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
     for _ in range(3):
-        spmm_device(t, b, out=out)
+        spmm_device(t, b, out=out, math=math)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(iters):
-        spmm_device(t, b, out=out)
+        spmm_device(t, b, out=out, math=math)
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / iters
@@ -60,8 +60,8 @@ def main():
     t1 = build_device(dp)
     after = spmm_ms(t1, b)
     print(f"{args.workload}: reorder {rt:.2f} s {info}")
-    print(f"  before: {base:.3f} ms {stats(t0)}")
-    print(f"  after : {after:.3f} ms {stats(t1)}")
+    print(f"  before: {base:.3f} ms (tensor cores {spmm_ms(t0, b, math='tc'):.3f} ms) {stats(t0)}")
+    print(f"  after : {after:.3f} ms (tensor cores {spmm_ms(t1, b, math='tc'):.3f} ms) {stats(t1)}")
 
 
 if __name__ == "__main__":

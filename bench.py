@@ -295,6 +295,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu DRAM-traffic measurement")
     ap.add_argument("--no-graph", action="store_true", help="time direct launches instead of CUDA graph replays")
+    ap.add_argument("--p2p-gather", action="store_true",
+                    help="N > 1: each rank's SpMM writes its C rows into rank 0's buffer over peer memory")
     ap.add_argument("--kernel-only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--math", default="auto", choices=["auto", "fp32", "tf32", "tc"])
     ap.add_argument("--sharded", action="store_true",

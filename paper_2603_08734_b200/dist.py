@@ -113,6 +113,28 @@ def gather_rows(c_local, cuts, rank: int, world: int, out=None):
     return None
 
 
+def share_from_rank0(t, rank: int):
+    """rank 0's CUDA tensor ``t`` mapped into every rank's address space through CUDA IPC (the
+    torch.multiprocessing reduction; peer access over NVLink between GPUs, or the same device
+    in another process).  Rank 0 gets ``t`` back; the others get a view of the same memory."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    obj = [reduce_tensor(t) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    if rank == 0:
+        return t
+    fn, args = obj[0]
+    return fn(*args)
+
+
+def spmm_rows_into(tile, b, c_full, r0: int, r1: int, **kw):
+    """This rank's shard SpMM with its C rows written straight into ``c_full`` (rank 0's full C,
+    possibly a peer-memory view): the epilogue's stores travel over NVLink, so no separate C
+    gather follows.  Rows [r0, r1) of c_full receive the shard's rows."""
+    from .device import spmm_device
+    return spmm_device(tile, b, out=c_full[r0:r1], **kw)
+
+
 # ---------------------------------------------------------------------------------------------
 # device shard build (one rank's part of the global format)
 # ---------------------------------------------------------------------------------------------
@@ -264,6 +286,22 @@ def run_sharded_bench(args, metric: str, clock_factory=None, config_factory=None
     torch.cuda.synchronize()
     bcast_ms = ev0.elapsed_time(ev1)
     out = torch.empty((r1 - r0, n_feat), dtype=torch.float32, device=dev)
+    # --p2p-gather: every rank's SpMM writes its C rows straight into rank 0's C over peer memory
+    # (CUDA IPC), so no gather follows; any failure to map the buffer falls back to NCCL
+    c_peer, p2p_note = None, None
+    if getattr(args, "p2p_gather", False) and world > 1:
+        try:
+            c_full = torch.empty((n, n_feat), dtype=torch.float32, device=dev) if rank == 0 else None
+            c_peer = share_from_rank0(c_full, rank)
+            p2p_note = "C rows stored by each rank's SpMM epilogue into rank 0's buffer over peer memory"
+        except Exception as exc:  # noqa: BLE001 -- the NCCL gather below still works
+            c_peer, p2p_note = None, f"peer mapping failed ({type(exc).__name__}); NCCL gather"
+        ok = torch.tensor([0.0 if c_peer is None else 1.0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1.0:
+            c_peer = None
+    if c_peer is not None:
+        out = c_peer[r0:r1]
     for _ in range(args.warmup):
         spmm_device(tile, b, out=out)
     dist.barrier()
@@ -298,7 +336,8 @@ def run_sharded_bench(args, metric: str, clock_factory=None, config_factory=None
     torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0.record()
-    gather_rows(out, cuts, rank, world)
+    if c_peer is None:
+        gather_rows(out, cuts, rank, world)
     c1.record()
     torch.cuda.synchronize()
     gather_ms = c0.elapsed_time(c1)
@@ -350,6 +389,7 @@ def run_sharded_bench(args, metric: str, clock_factory=None, config_factory=None
                         "b_values": "U(-1,1) drawn on rank 0's device, broadcast"},
             "gpu_launches": int(lsum.item()),
             "collectives": {"b_broadcast_ms": bcast_ms, "c_gather_ms": gather_ms,
+                            "c_placement": p2p_note or "NCCL point-to-point gather to rank 0",
                             "b_bytes": int(b.numel() * b.element_size()), "c_bytes": int(n * n_feat * 4)},
             "roofline": {"bound": "hbm", "achieved": alg_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg_bytes / (ms * 1e-3) / 1e9 / peak, "traffic": None,

@@ -359,7 +359,7 @@ def run_sharded_bench(args, metric: str, clock_factory=None, config_factory=None
     from .device import TILE_HOST_FIELDS, HostStream
     hs = HostStream({k: getattr(tile, k).cpu().pin_memory() for k in TILE_HOST_FIELDS}, b.cpu().pin_memory(),
                     tile.n_rows, tile.n_cols, tile.window_size, dev)
-    e2e_steps = max(2, min(args.steps, 6))
+    e2e_steps = max(2, int(getattr(args, "e2e_steps", 24)))
     hs.run(2)
     dist.barrier()
     e2e_ms = [hs.run(e2e_steps)]

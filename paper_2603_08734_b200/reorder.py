@@ -94,7 +94,7 @@ def permute_rows_device(a, order):
     from ._lib import call, lib
     from .device import DeviceCsr, _ptr, _stream, _ws
     dev = a.device
-    o = order if isinstance(order, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(order, np.int64))
+    o = order if isinstance(order, torch.Tensor) else torch.from_numpy(np.array(order, dtype=np.int64))
     o = o.to(device=dev, dtype=torch.int64)
     if o.numel() != a.n_rows:
         raise ValueError("order length must equal n_rows")
@@ -265,7 +265,7 @@ def permutation_objective(a: CsrMatrix, w: ColumnWeights, order) -> float:
     left to right)."""
     import torch
     ctx = _Ctx(a, w.alpha)
-    o = torch.from_numpy(np.ascontiguousarray(order, np.int64)).to(ctx.d.device)
+    o = torch.from_numpy(np.array(order, dtype=np.int64)).to(ctx.d.device)
     return ctx.objective(o)
 
 

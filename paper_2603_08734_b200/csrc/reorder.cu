@@ -382,8 +382,10 @@ int rsh_candidates(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_row
                    int32_t* cand_cnt, unsigned long long* stats, cudaStream_t st) {
   if (max_candidates < 1) return fail(kInvalid, "max_candidates must be at least 1");
   if (max_candidates > kKnnCap) return fail(kInvalid, "max_candidates above the device table (%d)", kKnnCap);
+  if (!stats) return fail(kInvalid, "rsh_candidates: null stats");
   RSH_CUDA(cudaMemsetAsync(stats, 0, sizeof(unsigned long long), st));
   if (!n_rows) return kOk;
+  if (!row_ptr || !at_row_ptr || !cand || !cand_cnt) return fail(kInvalid, "rsh_candidates: null array");
   const size_t smem = sizeof(KnnSmem) * kKnnWarps;
   RSH_CUDA(cudaFuncSetAttribute(k_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t blocks = (n_rows + kKnnWarps - 1) / kKnnWarps;

@@ -432,6 +432,7 @@ int rsh_csr_spmm_f64(const int64_t* row_ptr, const int32_t* col_idx, const float
                      const float* B, int64_t ldb, int64_t N, float* C, int64_t ldc, cudaStream_t st) {
   if (n_rows < 0 || N < 0 || ldb < N || ldc < N) return rsh::fail(rsh::kInvalid, "rsh_csr_spmm_f64: bad shape");
   if (n_rows == 0 || N == 0) return rsh::kOk;
+  if (!row_ptr || !B || !C) return rsh::fail(rsh::kInvalid, "rsh_csr_spmm_f64: null operand");
   int64_t blocks = (n_rows + 7) / 8;
   const int64_t cap = 32LL * rsh::sm_count();
   if (blocks > cap) blocks = cap;
@@ -443,6 +444,9 @@ int rsh_csr_spmm_f64(const int64_t* row_ptr, const int32_t* col_idx, const float
 // out (device uint64[2]) = [windows, occupied window rows]
 int rsh_tile_density(const int32_t* row_window_id, const int64_t* row_window_offset, int64_t n_entries,
                      const uint64_t* bitmaps, unsigned long long* out, cudaStream_t st) {
+  if (!out) return rsh::fail(rsh::kInvalid, "rsh_tile_density: null output");
+  if (n_entries > 0 && (!row_window_id || !row_window_offset || !bitmaps))
+    return rsh::fail(rsh::kInvalid, "rsh_tile_density: null format array");
   RSH_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st));
   if (n_entries <= 0) return rsh::kOk;
   rsh::k_tile_density<<<rsh::grid_1d(n_entries), rsh::kThreads, 0, st>>>(

@@ -774,7 +774,8 @@ int rsh_transpose_csr(const int64_t* row_ptr, const int32_t* col_idx, const floa
 int rsh_window_nnz(const int64_t* row_ptr, int64_t n_rows, const int32_t* win_start, const int32_t* win_count,
                    int64_t n_win, int32_t window_size, long long* out, cudaStream_t st) {
   if (!out) return fail(kInvalid, "rsh_window_nnz: null output");
-  if (n_win > 0 && (!row_ptr || !win_start || !win_count || window_size < 1 || n_rows < 0))
+  // win_count may be null: every window then spans min(window_size, rows left) rows
+  if (n_win > 0 && (!row_ptr || !win_start || (!win_count && window_size < 1) || n_rows < 0))
     return fail(kInvalid, "rsh_window_nnz: bad arguments");
   RSH_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), st));
   if (n_win <= 0) return kOk;

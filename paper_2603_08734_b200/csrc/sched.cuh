@@ -23,7 +23,7 @@ enum UnitType { kUnitWindow = 0, kUnitResidual = 1, kUnitZero = 2 };
 //         [5]=blocks per window unit (the fixed chunking) [6]=windows reduced by the fixup
 //         kernels (more than kTicketMax chunks) [7]=their first-level fix-up segments
 //         [8]=device address of the row-major window list (rsh_schedule_rowmajor), [9]=its tc nnz
-//         (0 = no list)
+//         (0 = no list), [11]=device address of its unit headers (k_unit_headers, 3 x int4 per unit)
 // counters: uint32 [0]=next unit [1]=warps done
 struct Sched {
   int64_t* header;

@@ -594,7 +594,52 @@ struct StreamSmem {
   int rend[kMaxRows + 1];          // row-major list end of each unit row
   long long rowoff[kMaxRows];      // element offset of each unit row in C (or the partials)
   UnitDesc u;
+  int4 nh[3];                      // the unit's header (k_unit_headers)
 };
+
+// Unit headers (schedule time, with the row-major list): everything the streaming kernel's unit
+// setup otherwise chases through four dependent loads (unit -> group row / slot / value start ->
+// bitmaps -> per-row totals), as three int4 per unit:
+//   [0] = {units.x (type | chunk << 2), group, first row, partial slot (-1: rows go to C)}
+//   [1] = {first list index, list entries, first block, end block}
+//   [2] = the 8 per-row list ends (inclusive prefix), 16 bits each
+// Residual and zero units keep their raw unit in [0] ([1], [2] zero).
+__global__ void k_unit_headers(Sched s, const unsigned long long* __restrict__ bitmaps, int4* __restrict__ hdr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_units = s.header[2];
+  for (int64_t u = warp0; u < n_units; u += nwarps) {
+    const int4 un = s.units[u];
+    if ((un.x & 3) != kUnitWindow) {
+      if (lane < 3) hdr[3 * u + lane] = lane == 0 ? un : make_int4(0, 0, 0, 0);
+      continue;
+    }
+    unsigned long long t0 = 0, t1 = 0;
+    for (int32_t blk = un.z + lane; blk < un.w; blk += 32) {
+      const unsigned long long bm = bitmaps[blk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        t0 += (unsigned long long)__popc(uint32_t(bm >> (8 * i)) & 0xffu) << (16 * i);
+        t1 += (unsigned long long)__popc(uint32_t(bm >> (8 * (i + 4))) & 0xffu) << (16 * i);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+    }
+    const unsigned long long rp0 = t0 * 0x0001000100010001ull;
+    const unsigned long long rp1 = t1 * 0x0001000100010001ull + (rp0 >> 48) * 0x0001000100010001ull;
+    if (lane == 0) {
+      const int32_t g = un.y, slot = s.grp_slot[g];
+      hdr[3 * u] = make_int4(un.x, g, s.grp_rid[g], slot < 0 ? -1 : slot + (un.x >> 2));
+      hdr[3 * u + 1] = make_int4(s.vstart[un.z], (int)(rp1 >> 48), un.z, un.w);
+      hdr[3 * u + 2] = make_int4((int)(uint32_t)rp0, (int)(uint32_t)(rp0 >> 32), (int)(uint32_t)rp1,
+                                 (int)(uint32_t)(rp1 >> 32));
+    }
+  }
+}
 
 // format-stream copy with an L2 policy (the nonzero stream is read once: evict_first)
 __device__ __forceinline__ void cp_async4_sp(uint32_t saddr, const void* g, uint64_t pol) {
@@ -948,6 +993,56 @@ __device__ __forceinline__ void stream_rows(const SpmmArgs& a, StreamSmem<kCap>&
   while (cur < r1) flush();
 }
 
+// cp.async of 16 bytes (a unit header word) into shared memory
+__device__ __forceinline__ void cp_async16_s(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+
+// A window unit's state from its header (k_unit_headers): row table, C / partial row offsets,
+// descriptor fields; the caller copies the list afterwards.
+template <int kCap>
+__device__ __forceinline__ void apply_header(const SpmmArgs& a, StreamSmem<kCap>& sm, const int2* ulist) {
+  const int lane = threadIdx.x & 31;
+  const int4 h0 = sm.nh[0], h1 = sm.nh[1];
+  const int64_t rid = h0.z;
+  const int32_t slot = h0.w;
+  if (lane < 8) {
+    const int4 h2 = sm.nh[2];
+    const uint32_t w = lane < 2 ? (uint32_t)h2.x : lane < 4 ? (uint32_t)h2.y : lane < 6 ? (uint32_t)h2.z : (uint32_t)h2.w;
+    sm.rend[lane] = (int)((w >> (16 * (lane & 1))) & 0xffffu);
+    sm.rowoff[lane] = slot < 0 ? (rid + lane) * a.ldc : ((int64_t)slot * 8 + lane) * a.N;
+  }
+  if (lane == 0) {
+    const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
+    sm.u.window = 1;
+    sm.u.to_part = slot >= 0;
+    sm.u.g = h0.y;
+    sm.u.slot = slot;
+    sm.u.rid = rid;
+    sm.u.avail = (int)avail;
+    sm.u.nrows = slot < 0 ? (int)avail : 8;
+    sm.u.v0 = h1.x;
+    sm.u.total = h1.y;
+    sm.u.b0 = h1.z;
+    sm.u.b1 = h1.w;
+    sm.u.ulist = ulist;
+  }
+  __syncwarp();
+}
+
+template <int kCap>
+__device__ __forceinline__ void list_copy(StreamSmem<kCap>& sm, uint64_t pol_a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(sm.list);
+  const int n = sm.u.total < kCap ? sm.u.total : kCap;
+  const int2* src = sm.u.ulist + sm.u.v0;
+  for (int p = lane; p < n; p += 32)
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(list_s + 8u * p),
+                 "l"(src + p), "l"(pol_a) : "memory");
+  cp_async_wait_all();
+  __syncwarp();
+}
+
 template <int VEC, class BT, int kDepth, int MINB, bool kFull, bool kNoL1, int kCap, int kG>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
   __shared__ StreamSmem<kCap> smem_all[kThreads / 32];
@@ -959,39 +1054,59 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
   const int n_fc = kG > 1 ? 1 : (a.N + 32 * VEC - 1) / (32 * VEC);
   const BT* B = reinterpret_cast<const BT*>(a.B);
   const uint64_t pol_b = policy_evict_last(), pol_a = policy_evict_first();
+  // list mode with unit headers: a unit's setup is one 48-byte header read plus its list copy
+  // instead of the chain unit -> group row / slot / value start -> bitmaps -> list (prefetching
+  // the next unit's header during this one measured no better).  Flags bit 7 keeps the chain.
+  const int2* ulist = (a.s.header[9] && !(a.flags & 4096)) ? reinterpret_cast<const int2*>(a.s.header[8]) : nullptr;
+  const int4* hdrs = (ulist && !(a.flags & 128)) ? reinterpret_cast<const int4*>(a.s.header[11]) : nullptr;
+  const uint32_t nh_s = (uint32_t)__cvta_generic_to_shared(sm.nh);
 
   uint32_t u = 0;
   if (lane == 0) u = atomicAdd(a.s.counters, 1u);
   u = __shfl_sync(0xffffffffu, u, 0);
   while ((int64_t)u < total_units) {
-    const int4 un = a.s.units[u];
+    int4 un;
+    if (hdrs) {
+      if (lane < 3) cp_async16_s(nh_s + 16u * lane, hdrs + 3 * (int64_t)u + lane);
+      cp_async_wait_all();
+      __syncwarp();
+      un = sm.nh[0];
+    } else {
+      un = a.s.units[u];
+    }
     // claim the next unit now: the atomic's round trip overlaps this unit's work
-    if (lane == 0) sm.u.next = atomicAdd(a.s.counters, 1u);
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(a.s.counters, 1u);
     const int type = un.x & 3;
     if (type == kUnitZero) {
       zero_rows<VEC>(a, un.y, un.z);
     } else {
       if (type == kUnitWindow) {
-        if (lane == 0) {
-          const int32_t g = un.y;
-          const int64_t rid = a.s.grp_rid[g];
-          const int32_t slot = a.s.grp_slot[g];
-          sm.u.window = 1;
-          sm.u.to_part = slot >= 0;
-          sm.u.g = g;
-          // chunk k of a multi-chunk window writes partial slot (slot + k)
-          sm.u.slot = slot < 0 ? -1 : slot + (un.x >> 2);
-          sm.u.rid = rid;
-          const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
-          sm.u.avail = (int)avail;
-          sm.u.nrows = slot < 0 ? (int)avail : 8;
-          sm.u.b0 = un.z;
-          sm.u.b1 = un.w;
-          sm.u.ulist = (a.s.header[9] && !(a.flags & 4096)) ? reinterpret_cast<const int2*>(a.s.header[8]) : nullptr;
-          sm.u.v0 = sm.u.ulist ? a.s.vstart[un.z] : 0;
+        if (hdrs) {
+          apply_header<kCap>(a, sm, ulist);
+          list_copy<kCap>(sm, pol_a);
+        } else {
+          if (lane == 0) {
+            const int32_t g = un.y;
+            const int64_t rid = a.s.grp_rid[g];
+            const int32_t slot = a.s.grp_slot[g];
+            sm.u.window = 1;
+            sm.u.to_part = slot >= 0;
+            sm.u.g = g;
+            // chunk k of a multi-chunk window writes partial slot (slot + k)
+            sm.u.slot = slot < 0 ? -1 : slot + (un.x >> 2);
+            sm.u.rid = rid;
+            const int64_t avail = a.window_size < a.n_rows - rid ? a.window_size : a.n_rows - rid;
+            sm.u.avail = (int)avail;
+            sm.u.nrows = slot < 0 ? (int)avail : 8;
+            sm.u.b0 = un.z;
+            sm.u.b1 = un.w;
+            sm.u.ulist = ulist;
+            sm.u.v0 = sm.u.ulist ? a.s.vstart[un.z] : 0;
+          }
+          __syncwarp();
+          window_fill<kCap>(a, sm, 0, pol_a);
         }
-        __syncwarp();
-        window_fill<kCap>(a, sm, 0, pol_a);
       } else {
         const int32_t i0 = un.y, i1 = un.z;
         const int nr = i1 - i0;
@@ -1021,8 +1136,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_stream(SpmmArgs a) {
         window_ticket_reduce<VEC, float>(a, sm.u.g, a.s.grp_slot[sm.u.g], sm.u.rid, sm.u.avail, n_fc);
     }
     __syncwarp();
-    u = sm.u.next;
-    __syncwarp();
+    u = __shfl_sync(0xffffffffu, nx, 0);
   }
   // last warp out rewinds the counters so the next launch needs no memset
   __syncwarp();
@@ -1229,6 +1343,7 @@ size_t rsh_rowmajor_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, i
   cv.take<unsigned long long>(mu);
   cv.take<unsigned long long>(mu);
   cv.take<int4>(mu);
+  cv.take<int4>(3 * mu);  // unit headers (k_unit_headers)
   size_t t = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                   (int4*)nullptr, (int4*)nullptr, (int)mu);
@@ -1274,6 +1389,7 @@ int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bit
   unsigned long long* keys = cv.take<unsigned long long>(s.max_units);
   unsigned long long* keys2 = cv.take<unsigned long long>(s.max_units);
   int4* units2 = cv.take<int4>(s.max_units);
+  int4* uhdr = cv.take<int4>(3 * s.max_units);
   size_t t = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                   (int4*)nullptr, (int4*)nullptr, (int)s.max_units);
@@ -1289,7 +1405,9 @@ int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bit
     RSH_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, keys, keys2, s.units, units2, (int)s.max_units, 0, 64, st));
     RSH_CUDA(cudaMemcpyAsync(s.units, units2, s.max_units * sizeof(int4), cudaMemcpyDeviceToDevice, st));
   }
-  const int64_t hdr[2] = {(int64_t)(uintptr_t)list, tc_nnz};
+  k_unit_headers<<<8 * sm_count(), kThreads, 0, st>>>(s, (const unsigned long long*)bitmaps, uhdr);
+  RSH_LAUNCHED("k_unit_headers");
+  const int64_t hdr[4] = {(int64_t)(uintptr_t)list, tc_nnz, 0, (int64_t)(uintptr_t)uhdr};
   RSH_CUDA(cudaMemcpyAsync(s.header + 8, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
   RSH_CUDA(cudaStreamSynchronize(st));  // hdr lives on this host stack frame
   return kOk;

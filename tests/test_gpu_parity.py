@@ -293,7 +293,8 @@ def test_permute_rows_matches_reference_semantics(small_corpus):
 
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
 def test_stream_kernel_bit_identical_across_variants(dtype):
-    """The streaming kernel's list pieces (kCap 256 / 320 / 448), pipeline depths and the row-walk
+    """The streaming kernel's list pieces (kCap 256 / 320 / 448), pipeline depths, unit setup (header
+    read or the chained lookups, flag 128) and the row-walk
     kernel accumulate every row in the same order: C must be bitwise equal across them for one
     schedule (and across lane-group splits of narrow rows, flag 2048),
     including multi-chunk windows (partials + ticket / fix-up reduction) and a near-dense row."""
@@ -315,7 +316,7 @@ def test_stream_kernel_bit_identical_across_variants(dtype):
             continue
         # 256-block units + row-major list (the default schedule): every stream variant agrees
         base = spmm_device(t, b, math="fp32", cc_variant=0)
-        for v in (8, 16, 24, 32, 40, 48, 1024, 2048):
+        for v in (8, 16, 24, 32, 40, 48, 128, 1024, 2048):
             got = spmm_device(t, b, math="fp32", cc_variant=v)
             assert torch.equal(got.view(torch.int32), base.view(torch.int32)), (n, v)
         # 32-block units (bitmap decode, flag 4096): the stream and the row walk agree -- the row

@@ -151,10 +151,11 @@ size_t rsh_partials_bytes(int64_t n_entries, int64_t partial_slots, int64_t n_fe
 
 /* ---- row-major window list (optional, once per schedule; no reference counterpart): the
  *      window units' nonzeros as int2 (col_id, value) pairs in stream order (the buffer,
- *      16-byte aligned, also holds the scratch that puts the window units longest-first; size
- *      it with rsh_rowmajor_bytes).  rsh_spmm_cc then copies each unit's list coalesced instead of
- *      decoding bitmaps; results are bit-identical with or without it.  The list must outlive
- *      the schedule's use (its address is recorded in the schedule). */
+ *      16-byte aligned, also holds the scratch that puts the window units longest-first and a
+ *      48-byte header per unit -- row, partial slot, list range, per-row list ends; size it with
+ *      rsh_rowmajor_bytes).  rsh_spmm_cc then sets a unit up from its header and copies its list
+ *      coalesced instead of decoding bitmaps; results are bit-identical with or without it.  The
+ *      buffer must outlive the schedule's use (its addresses are recorded in the schedule). */
 size_t rsh_rowmajor_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res, int64_t tc_nnz);
 int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
                           const float* tc_values, int64_t n_blocks, int64_t tc_nnz, int64_t n_res, void* sched,

@@ -143,6 +143,18 @@ int main(int argc, char** argv) {
         run(k_replay<8, 256>, c, "R8");
       }
     }
+    if (name[0] == 'c') {  // L1 capacity: the same gathers with the streaming kernel's 23 KB of
+                           // shared memory per CTA (and twice that) taken from the L1 carve-out
+      for (int kb : {23, 46}) {
+        auto run3 = [&](auto kern) {
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024));
+          const float ms = timeit([&] { kern<<<sms * 4, 256, kb * 1024>>>(B, idx, n, counter, out, nullptr, SEG); });
+          printf("  csr      R6  ctas/SM 4 smem %2d KB/CTA: %.3f ms\n", kb, ms);
+        };
+        if (RB == 512) run3(k_replay<6, 512>);
+        else run3(k_replay<6, 256>);
+      }
+    }
     if (name[0] == 'c') {  // unit-setup cost: dependent loads per segment, and longer segments
       int* chain;
       CK(cudaMalloc(&chain, 4 << 20));

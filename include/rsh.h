@@ -155,7 +155,11 @@ size_t rsh_partials_bytes(int64_t n_entries, int64_t partial_slots, int64_t n_fe
  *      48-byte header per unit -- row, partial slot, list range, per-row list ends; size it with
  *      rsh_rowmajor_bytes).  rsh_spmm_cc then sets a unit up from its header and copies its list
  *      coalesced instead of decoding bitmaps; results are bit-identical with or without it.  The
- *      buffer must outlive the schedule's use (its addresses are recorded in the schedule). */
+ *      buffer must outlive the schedule's use (its addresses are recorded in the schedule).  The
+ *      list is a SNAPSHOT of col_id and tc_values: rsh_spmm_cc then reads the pairs from it, not
+ *      from its own col_id / tc_values arguments, so a caller that changes the values (same
+ *      sparsity) must rebuild the list (paper_2603_08734_b200.device keys its cached plan on the
+ *      arrays' identity and version for this). */
 size_t rsh_rowmajor_bytes(int64_t n_rows, int64_t n_entries, int64_t n_blocks, int64_t n_res, int64_t tc_nnz);
 int rsh_schedule_rowmajor(int64_t n_rows, int64_t n_entries, const uint64_t* bitmaps, const int32_t* col_id,
                           const float* tc_values, int64_t n_blocks, int64_t tc_nnz, int64_t n_res, void* sched,
